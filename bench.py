@@ -1,0 +1,405 @@
+#!/usr/bin/env python
+"""PQTopK hot-path benchmark (B200).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4] [--impl ours|reference]
+    python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 bench.py --gpus N
+
+A step is one pass of the whole hot path over one batch: K1 sub-id scores
+(pq_subscores) -> K2 fused gather-sum-select -> K3 merge (pq_score_topk), and
+for N > 1 GPUs (item-sharded catalogue) an NCCL all-gather of the B x K local
+results followed by pq_merge_topk.  Metric (BASELINE.json): user-item
+scores/s = B * N_items / step time (whole job), plus top-K queries/s.
+
+Timing: W untimed warm-up steps; K timed steps bracketed by barrier +
+synchronize; each step timed with CUDA events on the launching stream; before
+each step a 256 MiB buffer is written (L2 flush, outside the events); the
+reported time is the max over ranks.  The roofline block uses the fused
+kernel's own launch time (events recorded by the library around K2).
+Rank 0 prints ONE JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import pqsynth  # noqa: E402
+
+FALLBACK_PEAKS = {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0, "source": "fallback (B200_PROFILING.md)"}
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        d["source"] = "measured (MEASURED_PEAKS.json)"
+        return d
+    return dict(FALLBACK_PEAKS)
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """NVML sampling of SM clock + throttle reasons during the timed region."""
+    REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown"}
+
+    def __init__(self, torch_dev: int):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            h = None
+            try:
+                import torch
+                uuid = str(torch.cuda.get_device_properties(torch_dev).uuid)
+                for i in range(pynvml.nvmlDeviceGetCount()):
+                    hh = pynvml.nvmlDeviceGetHandleByIndex(i)
+                    u = pynvml.nvmlDeviceGetUUID(hh)
+                    u = u.decode() if isinstance(u, bytes) else u
+                    if u.replace("GPU-", "") == uuid.replace("GPU-", ""):
+                        h = hh
+            except Exception:
+                h = None
+            if h is None:
+                vis = os.environ.get("CUDA_VISIBLE_DEVICES", "")
+                ids = [int(x) for x in vis.split(",") if x.strip().isdigit()]
+                h = pynvml.nvmlDeviceGetHandleByIndex(ids[torch_dev] if torch_dev < len(ids) else torch_dev)
+            self.h = h
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # pragma: no cover - no NVML
+            self.err = str(e)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            self._stop.wait(0.1)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.ok:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "note": "NVML unavailable"}
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------------------------- helpers
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def shard(N, world, rank):
+    n = N // world
+    lo = rank * n
+    hi = N if rank == world - 1 else lo + n
+    return lo, hi
+
+
+def workload_name(cfg):
+    return (f"{cfg.name}: N={cfg.N:,} m={cfg.m} b={cfg.b} d={cfg.d} B={cfg.B} K={cfg.K} "
+            f"codes={cfg.codes}")
+
+
+def cpu_oracle_sample(cfg, codes, S_host, gpu_ids, gpu_sc, budget_s=12.0, max_users=64):
+    """Time the CPU oracle (Alg. 1, plain C + OpenMP) on a bounded sample of
+    users over the full catalogue; also check those users bit-exactly."""
+    import oracle
+    done, t_tot, exact = 0, 0.0, 0
+    while done < min(max_users, cfg.B) and t_tot < budget_s:
+        u = done
+        t0 = time.perf_counter()
+        ids, sc = oracle.pq_topk(codes, S_host[u:u + 1], cfg.K)
+        t_tot += time.perf_counter() - t0
+        if gpu_ids is not None:
+            exact += int(np.array_equal(ids[0], gpu_ids[u]) and
+                         np.array_equal(sc[0].view(np.uint32), gpu_sc[u].view(np.uint32)))
+        done += 1
+    return {"value": done * cfg.N / t_tot, "unit": "user-item scores/s", "cores": oracle.max_threads(),
+            "kind": "oracle",
+            "sample": f"users 0..{done - 1} of {cfg.B} over all {cfg.N:,} items (Alg. 1 item-major, "
+                      f"fp32 k-ordered sums, heap top-K), {t_tot:.1f} s"}, done, exact
+
+
+# ----------------------------------------------------------------------------- reference arm
+def run_reference(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    import oracle
+    cfg = pqsynth.CONFIGS[args.config]
+    codes = pqsynth.codes(cfg)
+    P = pqsynth.psi(cfg)
+    F = pqsynth.phi(cfg)
+    # users per step: about 1 s of oracle work per step at ~1e9 lookups/s/core
+    lk = cfg.N * cfg.m
+    upstep = max(1, min(cfg.B, int(1.5e9 * oracle.max_threads() / max(lk, 1) / 4)))
+    S_all = None
+    times = []
+    for s in range(args.warmup + args.steps):
+        u0 = (s * upstep) % cfg.B
+        Fu = F[u0:u0 + upstep]
+        t0 = time.perf_counter()
+        S = oracle.subscores(Fu, P)                # Eq. 4 (fp64 -> fp32)
+        oracle.pq_topk(codes, S, cfg.K)            # Alg. 1 + TopK
+        dt = time.perf_counter() - t0
+        if s >= args.warmup:
+            times.append(dt)
+        S_all = S
+    del S_all
+    t = sum(times) / len(times)
+    value = upstep * cfg.N / t
+    line = {
+        "impl": "reference", "metric": "user-item scores/s", "value": value, "unit": "user-item scores/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
+        "higher_is_better": True, "scaling": "strong" if world > 1 else "weak", "vs_baseline": None,
+        "dtype": "f32", "data": "synthetic (pqsynth, seeded)",
+        "config": {"workload": workload_name(cfg), "users_per_step": upstep},
+        "cpu_baseline": {"value": value, "unit": "user-item scores/s", "cores": oracle.max_threads(),
+                         "kind": "oracle",
+                         "sample": f"{upstep} user(s) per step over all {cfg.N:,} items (K1 fp64 + Alg. 1)"},
+        "e2e": {"value": value, "unit": "user-item scores/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "queries_per_s": upstep / t,
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- our arm
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2408_09992_b200 as pq
+
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    pq.load_library()
+    cfg = pqsynth.CONFIGS[args.config]
+    B, K, m, b, d = cfg.B, cfg.K, cfg.m, cfg.b, cfg.d
+    lo, hi = shard(cfg.N, world, rank)
+    n_local = hi - lo
+
+    codes = pqsynth.codes(cfg, lo, hi)
+    P = pqsynth.psi(cfg)
+    F = pqsynth.phi(cfg)
+
+    t0 = time.perf_counter()
+    idx = pq.pq_create(codes, b=b, id_base=lo)
+    torch.cuda.synchronize()
+    create_s = time.perf_counter() - t0
+
+    F_d = torch.from_numpy(F).to(dev)
+    P_d = torch.from_numpy(P).to(dev)
+    S = torch.empty((B, m, b), dtype=torch.float32, device=dev)
+    ids = torch.empty((B, K), dtype=torch.int32, device=dev)
+    sc = torch.empty((B, K), dtype=torch.float32, device=dev)
+    ws = torch.empty(idx.topk_workspace_bytes(B, K), dtype=torch.uint8, device=dev)
+    if world > 1:
+        g_ids = torch.empty((world, B, K), dtype=torch.int32, device=dev)
+        g_sc = torch.empty((world, B, K), dtype=torch.float32, device=dev)
+        out_ids = torch.empty((B, K), dtype=torch.int32, device=dev)
+        out_sc = torch.empty((B, K), dtype=torch.float32, device=dev)
+        mws_n = int(pq.load_library().pq_merge_workspace_bytes(world, B, K))
+        mws = torch.empty(max(mws_n, 1), dtype=torch.uint8, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def step():
+        pq.pq_subscores(F_d, P_d, S)
+        pq.pq_score_topk(idx, S, K, ws=ws, ids=ids, scores=sc)
+        if world > 1:
+            dist.all_gather_into_tensor(g_ids, ids)
+            dist.all_gather_into_tensor(g_sc, sc)
+            pq.pq_merge_topk(g_ids, g_sc, ws=mws, out_ids=out_ids, out_scores=out_sc)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    # ------------------------------------------------------------- timed (device-resident)
+    idx.timing_enable(True)
+    idx.timing_read()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    sampler = ClockSampler(local)
+    n_launch0 = pq.launch_count()
+    with sampler:
+        barrier()
+        torch.cuda.synchronize()
+        for e0, e1 in evs:
+            flush.fill_(1)
+            e0.record()
+            step()
+            e1.record()
+        torch.cuda.synchronize()
+        barrier()
+    gpu_launches = pq.launch_count() - n_launch0
+    k2_ms, k3_ms, n_k2 = idx.timing_read()
+    idx.timing_enable(False)
+    step_ms = [a.elapsed_time(c) for a, c in evs]
+    tot_ms = sum(step_ms)
+    t = torch.tensor([tot_ms, k2_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    tot_ms_max, k2_ms_max = float(t[0]), float(t[1])
+    ms_per_step = tot_ms_max / args.steps
+    value = B * cfg.N / (ms_per_step / 1e3)
+
+    # ------------------------------------------------------------- e2e (host buffers)
+    F_h = torch.from_numpy(F).pin_memory()
+    P_h = torch.from_numpy(P).pin_memory()
+    ids_h = torch.empty((B, K), dtype=torch.int32).pin_memory()
+    sc_h = torch.empty((B, K), dtype=torch.float32).pin_memory()
+    sws = torch.empty(idx.search_workspace_bytes(B, d, K), dtype=torch.uint8, device=dev)
+
+    def e2e_step():
+        if world == 1:
+            pq.pq_search(idx, F_h, P_h, K, ws=sws, ids=ids_h, scores=sc_h)
+        else:
+            pq.pq_search(idx, F_h, P_h, K, ws=sws, ids=ids, scores=sc)
+            dist.all_gather_into_tensor(g_ids, ids)
+            dist.all_gather_into_tensor(g_sc, sc)
+            pq.pq_merge_topk(g_ids, g_sc, ws=mws, out_ids=out_ids, out_scores=out_sc)
+            ids_h.copy_(out_ids, non_blocking=True)
+            sc_h.copy_(out_sc, non_blocking=True)
+    for _ in range(max(1, args.warmup)):
+        e2e_step()
+    torch.cuda.synchronize()
+    evs2 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+            for _ in range(args.steps)]
+    barrier()
+    for e0, e1 in evs2:
+        flush.fill_(1)
+        e0.record()
+        e2e_step()
+        e1.record()
+    torch.cuda.synchronize()
+    barrier()
+    e2e_ms = sum(a.elapsed_time(c) for a, c in evs2)
+    t2 = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t2, op=dist.ReduceOp.MAX)
+    e2e_value = B * cfg.N / (float(t2[0]) / args.steps / 1e3)
+
+    # final results for parity sampling (rank 0 at N = 1)
+    res_ids = (out_ids if world > 1 else ids).cpu().numpy()
+    res_sc = (out_sc if world > 1 else sc).cpu().numpy()
+
+    if rank != 0:
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    pk = peaks()
+    nsm = torch.cuda.get_device_properties(dev).multi_processor_count
+    f_max = float(pk.get("sm_max_mhz", 1965.0))
+    peak_lookups = nsm * 32 * f_max * 1e6            # 32 four-byte smem lookups / clk / SM
+    k2_avg_s = (k2_ms_max / max(n_k2, 1)) / 1e3
+    lookups = B * n_local * m                        # algorithmic lookups per K2 launch
+    achieved = lookups / k2_avg_s
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", f"k2_traffic_{cfg.name}.json")
+    if os.path.exists(tp):
+        traffic = json.load(open(tp)).get("dram_bytes_per_launch")
+    roofline = {
+        "bound": "smem", "kernel": "k2_score_select (fused gather-sum-select)",
+        "achieved": achieved / 1e9, "peak": peak_lookups / 1e9, "unit": "G lookups/s",
+        "frac": achieved / peak_lookups, "traffic": traffic,
+        "achieved_GBps_smem": achieved * 4 / 1e9, "peak_GBps_smem": peak_lookups * 4 / 1e9,
+        "peak_source": f"{nsm} SMs x 32 banks x 4 B x {f_max:.0f} MHz (sm_max_mhz, {pk['source']})",
+        "per_launch": {"lookups": lookups, "algorithmic_hbm_bytes": n_local * m + B * m * b * 4 + B * K * 8,
+                       "k2_ms": k2_avg_s * 1e3},
+        "k2_share_of_step": (k2_ms_max / args.steps) / ms_per_step,
+        "hbm_frac_algorithmic": (n_local * m / k2_avg_s) / (pk["hbm_gbs"] * 1e9),
+    }
+    cpu = None
+    parity = None
+    if world == 1 and not args.no_cpu_baseline:
+        cpu, nu, nexact = cpu_oracle_sample(cfg, codes, S.cpu().numpy(), res_ids, res_sc)
+        parity = f"bit-exact vs oracle (given GPU S) on {nexact}/{nu} sampled users"
+    clocks = sampler.summary()
+    line = {
+        "metric": "user-item scores/s", "value": value, "unit": "user-item scores/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+        "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic (pqsynth, seeded; BASELINE.json config recipe)",
+        "config": {"workload": workload_name(cfg), "items_per_gpu": n_local,
+                   "parallelism": f"item-shard x{world}" if world > 1 else "single GPU",
+                   "l2": "256 MiB L2 flush before every timed step (outside events)"},
+        "queries_per_s": B / (ms_per_step / 1e3),
+        "e2e": {"value": e2e_value, "unit": "user-item scores/s",
+                "h2d_bytes_per_step": B * d * 4 + m * b * (d // m) * 4,
+                "d2h_bytes_per_step": B * K * 8},
+        "gpu_launches": gpu_launches,
+        "roofline": roofline,
+        "cpu_baseline": cpu,
+        "parity": parity,
+        "clocks": clocks,
+        "create_s": create_s,
+        "step_ms": {"median": statistics.median(step_ms), "min": min(step_ms), "max": max(step_ms)},
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c4", choices=sorted(pqsynth.CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        print("bench.py: --warmup must be >= 3", file=sys.stderr)
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,85 @@
+// K1 — sub-id score matrices (Eq. 4):
+//   S[u][k][g] = sum_{t < d/m} psi[k][g][t] * phi[u][k*d/m + t]
+// phi_k is the k-th contiguous chunk of phi.
+//
+// Precision (R5): fp32 x fp32 products are exact in fp64, so each
+// dot product is accumulated in fp64 and rounded to fp32 once.  This meets the
+// 1e-5 relative bound per entry (plain fp32 accumulation does not, near zero)
+// and in practice reproduces fl32(exact) bit for bit.
+//
+// Roofline: K1 does 2*B*b*d flops (C4: 0.27 GFLOP fp64) and writes B*m*b*4
+// bytes (C4: 16.8 MB) — a few microseconds next to K2's tens of milliseconds,
+// so it stays SIMT fp64 (TF32/BF16 tensor cores would break the tolerance; see
+// DESIGN.md "K1").
+//
+// Grid: (m, ceil(B/UB)); a block stages psi_k (b x TT tile, padded rows) and
+// phi_k for UB users in shared memory and produces the UB x b outputs.
+#include "pq_internal.cuh"
+
+namespace pq {
+
+constexpr int K1_UB = 16;     // users per block
+constexpr int K1_TT = 32;     // t-tile (columns of psi_k staged per pass)
+constexpr int K1_THREADS = 256;
+
+__global__ void __launch_bounds__(K1_THREADS)
+k1_subscores(const float* __restrict__ phi, const float* __restrict__ psi, int B, int d,
+             int m, int b, float* __restrict__ S) {
+    __shared__ float ps[256 * (K1_TT + 1)];
+    __shared__ float fs[K1_UB * K1_TT];
+    const int k = blockIdx.x;
+    const int u0 = blockIdx.y * K1_UB;
+    const int nu = min(K1_UB, B - u0);
+    const int dm = d / m;
+    const int nout = nu * b;
+    constexpr int PER = (K1_UB * 256 + K1_THREADS - 1) / K1_THREADS;   // <= 16
+    double acc[PER];
+#pragma unroll
+    for (int j = 0; j < PER; ++j) acc[j] = 0.0;
+
+    for (int t0 = 0; t0 < dm; t0 += K1_TT) {
+        const int tt = min(K1_TT, dm - t0);
+        __syncthreads();
+        for (int x = threadIdx.x; x < b * tt; x += K1_THREADS) {
+            int g = x / tt, t = x - g * tt;
+            ps[g * (K1_TT + 1) + t] = psi[((int64_t)k * b + g) * dm + t0 + t];
+        }
+        for (int x = threadIdx.x; x < nu * tt; x += K1_THREADS) {
+            int u = x / tt, t = x - u * tt;
+            fs[u * K1_TT + t] = phi[(int64_t)(u0 + u) * d + (int64_t)k * dm + t0 + t];
+        }
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < PER; ++j) {
+            int o = threadIdx.x + j * K1_THREADS;
+            if (o < nout) {
+                int u = o / b, g = o - u * b;
+                const float* pr = ps + g * (K1_TT + 1);
+                const float* fr = fs + u * K1_TT;
+                double a = acc[j];
+                for (int t = 0; t < tt; ++t)
+                    a = fma((double)pr[t], (double)fr[t], a);   // exact product, fp64 sum
+                acc[j] = a;
+            }
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+        int o = threadIdx.x + j * K1_THREADS;
+        if (o < nout) {
+            int u = o / b, g = o - u * b;
+            S[((int64_t)(u0 + u) * m + k) * b + g] = (float)acc[j];   // one rounding (RN)
+        }
+    }
+}
+
+void launch_subscores(const float* phi, const float* psi, int B, int d, int m, int b,
+                      float* S, cudaStream_t st) {
+    if (B <= 0) return;
+    dim3 grid(m, (unsigned)ceil_div(B, K1_UB));
+    k1_subscores<<<grid, K1_THREADS, 0, st>>>(phi, psi, B, d, m, b, S);
+    count_launch();
+    check_launch("k1_subscores");
+}
+
+}  // namespace pq

@@ -1,0 +1,198 @@
+// K3 — exact segmented top-K on 64-bit ranking keys (TopK of Alg. 1).
+//
+// One block selects the K largest keys of one segment of <= K3_SEG entries
+// that it stages in shared memory (8-bit MSD radix select: 8 histogram passes
+// over shared memory, then a compaction of the keys above the K-th).  The
+// survivors are either written as an unsorted key list (an intermediate
+// level) or bitonic-sorted and decoded into ids/scores (the final level).
+// Keys are unique (score bits + id), so the selected set — and hence the
+// output — is unique: any segmentation / level structure gives the same bits.
+#include "select_dev.cuh"
+
+namespace pq {
+
+constexpr int K3_THREADS = 512;
+
+struct SrcKeys {        // keys[u][e], row length L
+    const uint64_t* keys;
+    int64_t L;
+    __device__ __forceinline__ uint64_t get(int u, int64_t e) const { return keys[(int64_t)u * L + e]; }
+};
+struct SrcPairs {       // (ids, scores)[p][u][j], e = p*K + j
+    const int32_t* ids;
+    const float* sc;
+    int B, K;
+    __device__ __forceinline__ uint64_t get(int u, int64_t e) const {
+        int p = (int)(e / K), j = (int)(e - (int64_t)p * K);
+        int64_t o = ((int64_t)p * B + u) * K + j;
+        int32_t id = ids[o];
+        if (id < 0) return 0ull;
+        return make_key(sc[o] + 0.0f, (uint32_t)id);     // + 0.0f: -0 -> +0 (R2)
+    }
+};
+struct SrcRows {        // score row R[u][e], global id = id0 + e
+    const float* R;
+    int64_t ld;
+    uint32_t id0;
+    __device__ __forceinline__ uint64_t get(int u, int64_t e) const {
+        return make_key(R[(int64_t)u * ld + e] + 0.0f, id0 + (uint32_t)e);
+    }
+};
+
+// grid (B, n_sub).  Segment s of user u = entries [s*SEG, min(L, (s+1)*SEG)).
+// Final mode (out_ids != null, n_sub must be 1): sorted ids/scores [B][K].
+// Level mode: unsorted keys at out_keys[(u*out_lists + list_off + s)*K + j].
+template <class Src>
+__global__ void __launch_bounds__(K3_THREADS)
+k3_select(Src src, int64_t L, int K, int Kp, uint64_t* __restrict__ out_keys,
+          int64_t out_lists, int64_t list_off, int32_t* __restrict__ out_ids,
+          float* __restrict__ out_sc) {
+    extern __shared__ uint64_t smk[];
+    const int u = blockIdx.x;
+    const int s = blockIdx.y;
+    const int64_t e0 = (int64_t)s * K3_SEG;
+    const int n = (int)(L - e0 < (int64_t)K3_SEG ? L - e0 : (int64_t)K3_SEG);
+    uint64_t* keys = smk;                         // [n]
+    uint64_t* sel = smk + K3_SEG;                 // [Kp]  (Kp = pow2ceil(min(K, SEG)))
+    uint32_t* hist = reinterpret_cast<uint32_t*>(sel + Kp);   // [256]
+    uint32_t* sh = hist + 256;                    // [4]
+    const int tid = threadIdx.x;
+
+    for (int i = tid; i < n; i += blockDim.x) keys[i] = src.get(u, e0 + i);
+    for (int i = tid; i < Kp; i += blockDim.x) sel[i] = 0ull;
+    if (tid == 0) sh[2] = 0;
+    __syncthreads();
+
+    uint64_t kth = 0;
+    if (n > K) {
+        uint64_t prefix = 0;
+        uint32_t krem = (uint32_t)K;
+        for (int shift = 56; shift >= 0; shift -= 8) {
+            const uint64_t hmask = (shift == 56) ? 0ull : (~0ull << (shift + 8));
+            for (int i = tid; i < 256; i += blockDim.x) hist[i] = 0;
+            __syncthreads();
+            for (int i0 = 0; i0 < n; i0 += blockDim.x) {
+                int i = i0 + tid;
+                uint64_t v = i < n ? keys[i] : 0ull;
+                bool ok = (i < n) && ((v & hmask) == prefix);
+                hist_add(hist, ok, (uint32_t)(v >> shift) & 255u);
+            }
+            __syncthreads();
+            if (tid < 32) {
+                uint32_t dg, ab;
+                warp_find_digit(hist, krem, dg, ab);
+                if (tid == 0) { sh[0] = dg; sh[1] = ab; }
+            }
+            __syncthreads();
+            prefix |= (uint64_t)sh[0] << shift;
+            krem -= sh[1];
+        }
+        kth = prefix;
+    }
+    // keep keys > kth, plus kth itself when it is a real key (unique); the empty
+    // key 0 is never collected (padding is 0 anyway)
+    for (int i = tid; i < n; i += blockDim.x) {
+        uint64_t v = keys[i];
+        if (v != 0ull && v >= kth) {
+            uint32_t pos = atomicAdd(&sh[2], 1u);
+            sel[pos] = v;
+        }
+    }
+    __syncthreads();
+    if (out_ids) {
+        block_bitonic_desc(sel, Kp);
+        for (int j = tid; j < K; j += blockDim.x) {
+            uint64_t v = j < Kp ? sel[j] : 0ull;
+            out_ids[(int64_t)u * K + j] = v ? key_id(v) : -1;
+            out_sc[(int64_t)u * K + j] = v ? key_score(v) : -INFINITY;
+        }
+    } else {
+        uint64_t* o = out_keys + ((int64_t)u * out_lists + list_off + s) * K;
+        for (int j = tid; j < K; j += blockDim.x) o[j] = j < Kp ? sel[j] : 0ull;
+    }
+}
+
+static size_t k3_smem(int K) {
+    int Kp = pow2_ceil(std::min(K, K3_SEG));
+    return (size_t)K3_SEG * 8 + (size_t)Kp * 8 + 256 * 4 + 16;
+}
+
+template <class Src>
+static void launch_k3(Src src, int64_t L, int B, int K, uint64_t* out_keys, int64_t out_lists,
+                      int64_t list_off, int32_t* ids, float* sc, cudaStream_t st) {
+    static bool attr_done = false;          // benign race: idempotent attribute set
+    size_t smem = k3_smem(K);
+    if (!attr_done) {
+        PQ_CUDA(cudaFuncSetAttribute(k3_select<Src>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)(K3_SEG * 8 + PQTOPK_MAX_K * 8 + 256 * 4 + 16)));
+        attr_done = true;
+    }
+    int n_sub = (int)ceil_div(L, K3_SEG);
+    dim3 grid((unsigned)B, (unsigned)n_sub);
+    int Kp = pow2_ceil(std::min(K, K3_SEG));
+    k3_select<Src><<<grid, K3_THREADS, smem, st>>>(src, L, K, Kp, out_keys, out_lists, list_off,
+                                                   ids, sc);
+    count_launch();
+    check_launch("k3_select");
+}
+
+size_t k3_reduce_scratch_bytes(int64_t L, int B, int K) {
+    if (L <= K3_SEG) return 0;
+    int64_t n_sub = ceil_div(L, K3_SEG);
+    return 2 * align_up((size_t)B * n_sub * K * 8, 256);
+}
+
+void k3_keys_to_topk(const uint64_t* keys, int64_t L, int B, int K, void* scratch,
+                     int32_t* ids, float* scores, cudaStream_t st) {
+    if (B <= 0 || K <= 0) return;
+    const uint64_t* cur = keys;
+    int64_t curL = L;
+    size_t half = L > K3_SEG ? align_up((size_t)B * ceil_div(L, K3_SEG) * K * 8, 256) : 0;
+    uint64_t* bufs[2] = {reinterpret_cast<uint64_t*>(scratch),
+                         reinterpret_cast<uint64_t*>(reinterpret_cast<char*>(scratch) + half)};
+    int pp = 0;
+    while (curL > K3_SEG) {
+        int64_t n_sub = ceil_div(curL, K3_SEG);
+        uint64_t* out = bufs[pp];
+        launch_k3(SrcKeys{cur, curL}, curL, B, K, out, n_sub, 0, nullptr, nullptr, st);
+        cur = out;
+        curL = n_sub * K;
+        pp ^= 1;
+    }
+    launch_k3(SrcKeys{cur, curL}, curL, B, K, nullptr, 0, 0, ids, scores, st);
+}
+
+size_t k3_pairs_scratch_bytes(int P, int B, int K) {
+    int64_t L = (int64_t)P * K;
+    if (L <= K3_SEG) return 0;
+    int64_t n_sub = ceil_div(L, K3_SEG);
+    size_t first = align_up((size_t)B * n_sub * K * 8, 256);
+    return first + k3_reduce_scratch_bytes(n_sub * K, B, K);
+}
+
+void k3_pairs_to_topk(const int32_t* ids_in, const float* sc_in, int P, int B, int K,
+                      void* scratch, int32_t* ids, float* scores, cudaStream_t st) {
+    if (B <= 0 || K <= 0) return;
+    int64_t L = (int64_t)P * K;
+    SrcPairs src{ids_in, sc_in, B, K};
+    if (L <= K3_SEG) {
+        launch_k3(src, L, B, K, nullptr, 0, 0, ids, scores, st);
+        return;
+    }
+    int64_t n_sub = ceil_div(L, K3_SEG);
+    uint64_t* lvl = reinterpret_cast<uint64_t*>(scratch);
+    size_t first = align_up((size_t)B * n_sub * K * 8, 256);
+    launch_k3(src, L, B, K, lvl, n_sub, 0, nullptr, nullptr, st);
+    k3_keys_to_topk(lvl, n_sub * K, B, K, reinterpret_cast<char*>(scratch) + first, ids, scores, st);
+}
+
+int k3_rows_lists(int64_t n) { return (int)ceil_div(n, K3_SEG); }
+
+void k3_rows_to_keys(const float* R, int64_t ld, int64_t n, int B, int K, uint32_t id0,
+                     uint64_t* out, int64_t out_lists_per_user, int64_t list_off,
+                     cudaStream_t st) {
+    if (B <= 0 || K <= 0 || n <= 0) return;
+    launch_k3(SrcRows{R, ld, id0}, n, B, K, out, out_lists_per_user, list_off, nullptr, nullptr, st);
+}
+
+}  // namespace pq

@@ -1,0 +1,462 @@
+// pq_abi.cu — the extern "C" boundary of libpqtopk.so (include/pqtopk.h).
+// Argument validation, index lifetime, workspace planning and dispatch to the
+// kernels K0..K4.  No exception crosses the ABI.
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <vector>
+
+#include "pq_internal.cuh"
+
+namespace pq {
+
+static thread_local std::string t_err;
+std::atomic<int64_t> g_launches{0};
+
+void set_error(const std::string& msg) { t_err = msg; }
+void clear_error() { t_err.clear(); }
+[[noreturn]] void fail(pq_status st, const std::string& msg) { throw Error{st, msg}; }
+void check_cuda(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) fail(PQ_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+void check_launch(const char* what) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) fail(PQ_ERR_CUDA, std::string("launch ") + what + ": " + cudaGetErrorString(e));
+}
+
+static bool is_device_ptr(const void* p) {
+    cudaPointerAttributes at;
+    cudaError_t e = cudaPointerGetAttributes(&at, p);
+    if (e != cudaSuccess) { cudaGetLastError(); return false; }
+    return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+static void need(bool c, const char* msg) {
+    if (!c) fail(PQ_ERR_INVALID_ARG, msg);
+}
+
+static int round_up4(int m) { return (m + 3) / 4 * 4; }
+
+// Workspace carving helper.
+struct Carve {
+    char* base;
+    size_t off = 0;
+    explicit Carve(void* p) : base(static_cast<char*>(p)) {}
+    template <class T> T* take(size_t bytes) {
+        T* r = reinterpret_cast<T*>(base ? base + off : nullptr);
+        off += align_up(bytes, 256);
+        return r;
+    }
+};
+
+struct TopkWs {
+    K2Plan plan;
+    size_t lanebuf, cand, k3, total;
+};
+static TopkWs topk_ws(const pq_index_s* idx, int B, int K) {
+    TopkWs w{};
+    w.plan = plan_k2(idx, B, K);
+    w.lanebuf = align_up(w.plan.lanebuf_bytes, 256);
+    w.cand = align_up(w.plan.cand_bytes, 256);
+    w.k3 = align_up(k3_reduce_scratch_bytes((int64_t)w.plan.chunks * K, B, K), 256);
+    w.total = w.lanebuf + w.cand + w.k3;
+    return w;
+}
+
+static void run_score_topk(pq_index_s* idx, const float* S, int B, int K, void* ws, size_t ws_bytes,
+                           int32_t* ids, float* scores, cudaStream_t st) {
+    TopkWs w = topk_ws(idx, B, K);
+    if (!ws || ws_bytes < w.total)
+        fail(PQ_ERR_WORKSPACE, "workspace too small: need " + std::to_string(w.total) + " bytes");
+    Carve c(ws);
+    uint64_t* lanebuf = c.take<uint64_t>(w.plan.lanebuf_bytes);
+    uint64_t* cand = c.take<uint64_t>(w.plan.cand_bytes);
+    void* k3s = c.take<char>(k3_reduce_scratch_bytes((int64_t)w.plan.chunks * K, B, K));
+    pq_index_s::EvTriple ev{};
+    if (idx->timing) {
+        PQ_CUDA(cudaEventCreate(&ev.a)); PQ_CUDA(cudaEventCreate(&ev.b)); PQ_CUDA(cudaEventCreate(&ev.c));
+        PQ_CUDA(cudaEventRecord(ev.a, st));
+    }
+    launch_k2(idx, w.plan, S, B, K, lanebuf, cand, st);
+    if (idx->timing) PQ_CUDA(cudaEventRecord(ev.b, st));
+    k3_keys_to_topk(cand, (int64_t)w.plan.chunks * K, B, K, k3s, ids, scores, st);
+    if (idx->timing) {
+        PQ_CUDA(cudaEventRecord(ev.c, st));
+        idx->events->push_back(ev);
+    }
+}
+
+static void check_topk_args(int B, int K) {
+    need(B >= 0, "B must be >= 0");
+    need(K >= 0, "K must be >= 0");
+    if (K > PQTOPK_MAX_K) fail(PQ_ERR_UNSUPPORTED, "K exceeds PQTOPK_MAX_K (4096)");
+}
+
+static int64_t dense_chunk(int64_t N, int B) {
+    const int64_t budget = (int64_t)1 << 30;             // bytes of fp32 scores per chunk
+    int64_t nc = budget / ((int64_t)std::max(B, 1) * 4);
+    nc = std::max<int64_t>(nc / K3_SEG * K3_SEG, K3_SEG);
+    return std::min(N, nc);
+}
+static int64_t dense_lists(int64_t N, int64_t nc) {
+    int64_t lists = 0;
+    for (int64_t c0 = 0; c0 < N; c0 += nc) lists += k3_rows_lists(std::min(nc, N - c0));
+    return lists;
+}
+
+static int recjpq_users(int64_t N, int B) {
+    int64_t bc = ((int64_t)1 << 30) / (N * 4);
+    return (int)std::max<int64_t>(1, std::min<int64_t>(B, bc));
+}
+
+}  // namespace pq
+
+using namespace pq;
+
+#define PQ_API_BEGIN try { clear_error();
+#define PQ_API_END                                                         \
+    }                                                                      \
+    catch (const pq::Error& e) { set_error(e.msg); return e.st; }          \
+    catch (const std::bad_alloc&) { set_error("host out of memory"); return PQ_ERR_OUT_OF_MEMORY; } \
+    catch (const std::exception& e) { set_error(e.what()); return PQ_ERR_CUDA; } \
+    catch (...) { set_error("unknown error"); return PQ_ERR_CUDA; }         \
+    return PQ_OK;
+
+extern "C" {
+
+int32_t pq_abi_version(void) { return PQTOPK_ABI_VERSION; }
+const char* pq_last_error(void) { return t_err.c_str(); }
+int64_t pq_launch_count(void) { return g_launches.load(); }
+
+pq_status pq_create(const uint8_t* codes, int64_t N, int32_t m, int32_t b, int64_t id_base,
+                    void* stream, pq_index* out) {
+    PQ_API_BEGIN
+    need(out != nullptr, "out is NULL");
+    *out = nullptr;
+    need(codes != nullptr, "codes is NULL");
+    need(N >= 1, "N must be >= 1");
+    need(m >= 1 && m <= 64, "m must be in [1, 64]");
+    need(b >= 1 && b <= 256, "b must be in [1, 256] (uint8 codes)");
+    need(id_base >= 0 && id_base + N <= 2147483647LL, "id_base + N must be <= 2^31 - 1");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+
+    pq_index_s* idx = new pq_index_s();
+    uint8_t* tmp = nullptr;
+    unsigned long long* d_bad = nullptr;
+    try {
+        idx->N = N; idx->m = m; idx->b = b; idx->id_base = id_base;
+        PQ_CUDA(cudaGetDevice(&idx->device));
+        PQ_CUDA(cudaDeviceGetAttribute(&idx->num_sms, cudaDevAttrMultiProcessorCount, idx->device));
+        int optin = 0;
+        PQ_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, idx->device));
+        idx->smem_optin = (size_t)optin;
+        idx->lay.mp = round_up4(m);
+        idx->lay.paired = 0;
+        idx->n_rows = N;
+        const size_t bytes = (size_t)N * idx->lay.mp + 64;
+        if (cudaMalloc(&idx->d_codes, bytes) != cudaSuccess) {
+            cudaGetLastError();
+            idx->d_codes = nullptr;
+            fail(PQ_ERR_OUT_OF_MEMORY, "cudaMalloc of " + std::to_string(bytes) + " code bytes failed");
+        }
+        PQ_CUDA(cudaMemsetAsync(idx->d_codes, 0, bytes, st));
+        const uint8_t* src = codes;
+        if (!is_device_ptr(codes)) {
+            if (cudaMalloc(&tmp, (size_t)N * m) != cudaSuccess) {
+                cudaGetLastError();
+                tmp = nullptr;
+                fail(PQ_ERR_OUT_OF_MEMORY, "cudaMalloc of the code staging buffer failed");
+            }
+            PQ_CUDA(cudaMemcpyAsync(tmp, codes, (size_t)N * m, cudaMemcpyHostToDevice, st));
+            src = tmp;
+        }
+        PQ_CUDA(cudaMalloc(&d_bad, sizeof(unsigned long long)));
+        PQ_CUDA(cudaMemsetAsync(d_bad, 0xFF, sizeof(unsigned long long), st));
+        launch_relayout(src, N, m, b, idx->d_codes, idx->lay.mp, d_bad, st);
+        unsigned long long bad = 0;
+        PQ_CUDA(cudaMemcpyAsync(&bad, d_bad, sizeof(bad), cudaMemcpyDeviceToHost, st));
+        PQ_CUDA(cudaStreamSynchronize(st));
+        if (bad != ~0ull) {
+            uint8_t v = 0;
+            PQ_CUDA(cudaMemcpy(&v, src + bad, 1, cudaMemcpyDeviceToHost));
+            char msg[160];
+            snprintf(msg, sizeof msg, "code out of range: item %lld split %lld has code %u >= b = %d",
+                     (long long)(bad / m), (long long)(bad % m), (unsigned)v, b);
+            fail(PQ_ERR_CODE_RANGE, msg);
+        }
+        if (tmp) { cudaFree(tmp); tmp = nullptr; }
+        cudaFree(d_bad);
+        d_bad = nullptr;
+    } catch (...) {
+        if (tmp) cudaFree(tmp);
+        if (d_bad) cudaFree(d_bad);
+        if (idx->d_codes) cudaFree(idx->d_codes);
+        delete idx;
+        throw;
+    }
+    *out = idx;
+    PQ_API_END
+}
+
+pq_status pq_destroy(pq_index idx) {
+    PQ_API_BEGIN
+    if (!idx) return PQ_OK;
+    cudaDeviceSynchronize();
+    if (idx->d_codes) cudaFree(idx->d_codes);
+    if (idx->d_perm) cudaFree(idx->d_perm);
+    if (idx->d_cmap) cudaFree(idx->d_cmap);
+    if (idx->events) {
+        for (auto& e : *idx->events) { cudaEventDestroy(e.a); cudaEventDestroy(e.b); cudaEventDestroy(e.c); }
+        delete idx->events;
+    }
+    delete idx;
+    PQ_API_END
+}
+
+pq_status pq_index_info(pq_index idx, int64_t* N, int32_t* m, int32_t* b, int64_t* id_base) {
+    PQ_API_BEGIN
+    need(idx != nullptr, "index is NULL");
+    if (N) *N = idx->N;
+    if (m) *m = idx->m;
+    if (b) *b = idx->b;
+    if (id_base) *id_base = idx->id_base;
+    PQ_API_END
+}
+
+pq_status pq_set_tuning(pq_index idx, const pq_tuning* t) {
+    PQ_API_BEGIN
+    need(idx != nullptr, "index is NULL");
+    if (t) {
+        need(t->warps >= 0 && t->warps <= 16, "tuning.warps must be in [0, 16]");
+        need(t->ctas >= 0 && t->chunks >= 0 && t->variant >= 0, "tuning values must be >= 0");
+        need(t->users_per_row >= 0 && t->users_per_row <= 32, "tuning.users_per_row must be in [0, 32]");
+        idx->tuning = *t;
+    } else {
+        idx->tuning = pq_tuning{};
+    }
+    PQ_API_END
+}
+
+pq_status pq_subscores(const float* seq_emb, const float* subitem_emb, int32_t B, int32_t d,
+                       int32_t m, int32_t b, float* S, void* stream) {
+    PQ_API_BEGIN
+    need(B >= 0, "B must be >= 0");
+    need(m >= 1 && m <= 64, "m must be in [1, 64]");
+    need(b >= 1 && b <= 256, "b must be in [1, 256]");
+    need(d >= m && d % m == 0, "d must be a positive multiple of m");
+    if (B == 0) return PQ_OK;
+    need(seq_emb && subitem_emb && S, "NULL pointer");
+    launch_subscores(seq_emb, subitem_emb, B, d, m, b, S, static_cast<cudaStream_t>(stream));
+    PQ_API_END
+}
+
+size_t pq_topk_workspace_bytes(pq_index idx, int32_t B, int32_t K) {
+    try {
+        if (!idx || B <= 0 || K <= 0 || K > PQTOPK_MAX_K) return 0;
+        return topk_ws(idx, B, K).total;
+    } catch (const pq::Error& e) {
+        set_error(e.msg);
+        return 0;
+    }
+}
+
+pq_status pq_score_topk(pq_index idx, const float* S, int32_t B, int32_t K, void* ws,
+                        size_t ws_bytes, int32_t* ids, float* scores, void* stream) {
+    PQ_API_BEGIN
+    need(idx != nullptr, "index is NULL");
+    check_topk_args(B, K);
+    if (B == 0 || K == 0) return PQ_OK;
+    need(S && ids && scores, "NULL pointer");
+    run_score_topk(idx, S, B, K, ws, ws_bytes, ids, scores, static_cast<cudaStream_t>(stream));
+    PQ_API_END
+}
+
+size_t pq_search_workspace_bytes(pq_index idx, int32_t B, int32_t d, int32_t K) {
+    try {
+        if (!idx || B <= 0 || K <= 0 || K > PQTOPK_MAX_K || d < idx->m || d % idx->m) return 0;
+        size_t s = 0;
+        s += align_up((size_t)B * idx->m * idx->b * 4, 256);      // S
+        s += align_up((size_t)B * d * 4, 256);                     // phi staging
+        s += align_up((size_t)idx->b * d * 4, 256);                // psi staging
+        s += 2 * align_up((size_t)B * K * 4, 256);                 // output staging
+        return s + topk_ws(idx, B, K).total;
+    } catch (const pq::Error& e) {
+        set_error(e.msg);
+        return 0;
+    }
+}
+
+pq_status pq_search(pq_index idx, const float* seq_emb, const float* subitem_emb, int32_t B,
+                    int32_t d, int32_t K, void* ws, size_t ws_bytes, int32_t* ids, float* scores,
+                    void* stream) {
+    PQ_API_BEGIN
+    need(idx != nullptr, "index is NULL");
+    check_topk_args(B, K);
+    need(d >= idx->m && d % idx->m == 0, "d must be a positive multiple of m");
+    if (B == 0 || K == 0) return PQ_OK;
+    need(seq_emb && subitem_emb && ids && scores, "NULL pointer");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const size_t need_bytes = pq_search_workspace_bytes(idx, B, d, K);
+    if (!ws || ws_bytes < need_bytes)
+        fail(PQ_ERR_WORKSPACE, "workspace too small: need " + std::to_string(need_bytes) + " bytes");
+    const int m = idx->m, b = idx->b;
+    Carve c(ws);
+    float* S = c.take<float>((size_t)B * m * b * 4);
+    float* phi_st = c.take<float>((size_t)B * d * 4);
+    float* psi_st = c.take<float>((size_t)b * d * 4);
+    int32_t* ids_st = c.take<int32_t>((size_t)B * K * 4);
+    float* sc_st = c.take<float>((size_t)B * K * 4);
+    char* rest = c.base + c.off;
+    const float* phi = seq_emb;
+    const float* psi = subitem_emb;
+    if (!is_device_ptr(seq_emb)) {
+        PQ_CUDA(cudaMemcpyAsync(phi_st, seq_emb, (size_t)B * d * 4, cudaMemcpyHostToDevice, st));
+        phi = phi_st;
+    }
+    if (!is_device_ptr(subitem_emb)) {
+        PQ_CUDA(cudaMemcpyAsync(psi_st, subitem_emb, (size_t)b * d * 4, cudaMemcpyHostToDevice, st));
+        psi = psi_st;
+    }
+    const bool host_ids = !is_device_ptr(ids), host_sc = !is_device_ptr(scores);
+    launch_subscores(phi, psi, B, d, m, b, S, st);
+    run_score_topk(idx, S, B, K, rest, ws_bytes - c.off, host_ids ? ids_st : ids,
+                   host_sc ? sc_st : scores, st);
+    if (host_ids) PQ_CUDA(cudaMemcpyAsync(ids, ids_st, (size_t)B * K * 4, cudaMemcpyDeviceToHost, st));
+    if (host_sc) PQ_CUDA(cudaMemcpyAsync(scores, sc_st, (size_t)B * K * 4, cudaMemcpyDeviceToHost, st));
+    if (host_ids || host_sc) PQ_CUDA(cudaStreamSynchronize(st));
+    PQ_API_END
+}
+
+size_t pq_merge_workspace_bytes(int32_t P, int32_t B, int32_t K) {
+    if (P <= 0 || B <= 0 || K <= 0 || K > PQTOPK_MAX_K) return 0;
+    return k3_pairs_scratch_bytes(P, B, K);
+}
+
+pq_status pq_merge_topk(const int32_t* ids, const float* scores, int32_t P, int32_t B, int32_t K,
+                        void* ws, size_t ws_bytes, int32_t* out_ids, float* out_scores,
+                        void* stream) {
+    PQ_API_BEGIN
+    need(P >= 1, "P must be >= 1");
+    check_topk_args(B, K);
+    if (B == 0 || K == 0) return PQ_OK;
+    need(ids && scores && out_ids && out_scores, "NULL pointer");
+    const size_t nb = pq_merge_workspace_bytes(P, B, K);
+    if (nb && (!ws || ws_bytes < nb))
+        fail(PQ_ERR_WORKSPACE, "workspace too small: need " + std::to_string(nb) + " bytes");
+    k3_pairs_to_topk(ids, scores, P, B, K, ws, out_ids, out_scores, static_cast<cudaStream_t>(stream));
+    PQ_API_END
+}
+
+pq_status pq_reconstruct(pq_index idx, const float* subitem_emb, int32_t d, float* W, void* stream) {
+    PQ_API_BEGIN
+    need(idx != nullptr, "index is NULL");
+    need(d >= idx->m && d % idx->m == 0, "d must be a positive multiple of m");
+    need(subitem_emb && W, "NULL pointer");
+    launch_reconstruct(idx, subitem_emb, d, W, static_cast<cudaStream_t>(stream));
+    PQ_API_END
+}
+
+size_t pq_dense_workspace_bytes(int64_t N, int32_t B, int32_t K) {
+    if (N <= 0 || B <= 0 || K <= 0 || K > PQTOPK_MAX_K) return 0;
+    const int64_t nc = dense_chunk(N, B);
+    const int64_t lists = dense_lists(N, nc);
+    return align_up((size_t)B * nc * 4, 256) + align_up((size_t)B * lists * K * 8, 256) +
+           k3_reduce_scratch_bytes(lists * K, B, K);
+}
+
+pq_status pq_dense_topk(const float* W, int64_t N, int32_t d, const float* seq_emb, int32_t B,
+                        int32_t K, int64_t id_base, void* ws, size_t ws_bytes, int32_t* ids,
+                        float* scores, void* stream) {
+    PQ_API_BEGIN
+    need(N >= 1 && d >= 1, "N and d must be >= 1");
+    need(id_base >= 0 && id_base + N <= 2147483647LL, "id_base + N must be <= 2^31 - 1");
+    check_topk_args(B, K);
+    if (B == 0 || K == 0) return PQ_OK;
+    need(W && seq_emb && ids && scores, "NULL pointer");
+    const size_t nb = pq_dense_workspace_bytes(N, B, K);
+    if (!ws || ws_bytes < nb) fail(PQ_ERR_WORKSPACE, "workspace too small: need " + std::to_string(nb) + " bytes");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int64_t nc = dense_chunk(N, B);
+    const int64_t lists = dense_lists(N, nc);
+    Carve c(ws);
+    float* R = c.take<float>((size_t)B * nc * 4);
+    uint64_t* keys = c.take<uint64_t>((size_t)B * lists * K * 8);
+    void* k3s = c.take<char>(k3_reduce_scratch_bytes(lists * K, B, K));
+    int64_t off = 0;
+    for (int64_t c0 = 0; c0 < N; c0 += nc) {
+        const int64_t n = std::min(nc, N - c0);
+        dense_sgemm(W + c0 * d, n, d, seq_emb, B, R, st);
+        k3_rows_to_keys(R, n, n, B, K, (uint32_t)(id_base + c0), keys, lists, off, st);
+        off += k3_rows_lists(n);
+    }
+    k3_keys_to_topk(keys, lists * K, B, K, k3s, ids, scores, st);
+    PQ_API_END
+}
+
+size_t pq_recjpq_workspace_bytes(pq_index idx, int32_t B, int32_t K) {
+    if (!idx || B <= 0 || K <= 0 || K > PQTOPK_MAX_K) return 0;
+    const int bc = recjpq_users(idx->N, B);
+    const int64_t lists = k3_rows_lists(idx->N);
+    return align_up((size_t)bc * idx->N * 4, 256) + align_up((size_t)B * lists * K * 8, 256) +
+           k3_reduce_scratch_bytes(lists * K, B, K);
+}
+
+pq_status pq_recjpq_topk(pq_index idx, const float* S, int32_t B, int32_t K, void* ws,
+                         size_t ws_bytes, int32_t* ids, float* scores, void* stream) {
+    PQ_API_BEGIN
+    need(idx != nullptr, "index is NULL");
+    check_topk_args(B, K);
+    if (B == 0 || K == 0) return PQ_OK;
+    need(S && ids && scores, "NULL pointer");
+    const size_t nb = pq_recjpq_workspace_bytes(idx, B, K);
+    if (!ws || ws_bytes < nb) fail(PQ_ERR_WORKSPACE, "workspace too small: need " + std::to_string(nb) + " bytes");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int bc = recjpq_users(idx->N, B);
+    const int64_t lists = k3_rows_lists(idx->N);
+    Carve c(ws);
+    float* R = c.take<float>((size_t)bc * idx->N * 4);
+    uint64_t* keys = c.take<uint64_t>((size_t)B * lists * K * 8);
+    void* k3s = c.take<char>(k3_reduce_scratch_bytes(lists * K, B, K));
+    for (int u0 = 0; u0 < B; u0 += bc) {
+        const int n = std::min(bc, B - u0);
+        PQ_CUDA(cudaMemsetAsync(R, 0, (size_t)n * idx->N * 4, st));    // "initialised to 0"
+        for (int k = 0; k < idx->m; ++k)                                  // "Not parallelised"
+            launch_recjpq_split(idx, S, B, u0, n, k, R, st);
+        k3_rows_to_keys(R, idx->N, idx->N, n, K, (uint32_t)idx->id_base, keys + (size_t)u0 * lists * K,
+                        lists, 0, st);
+    }
+    k3_keys_to_topk(keys, lists * K, B, K, k3s, ids, scores, st);
+    PQ_API_END
+}
+
+pq_status pq_timing_enable(pq_index idx, int32_t on) {
+    PQ_API_BEGIN
+    need(idx != nullptr, "index is NULL");
+    idx->timing = on ? 1 : 0;
+    if (on && !idx->events) idx->events = new std::vector<pq_index_s::EvTriple>();
+    PQ_API_END
+}
+
+pq_status pq_timing_read(pq_index idx, double* k2_ms, double* k3_ms, int64_t* launches) {
+    PQ_API_BEGIN
+    need(idx != nullptr, "index is NULL");
+    double t2 = 0.0, t3 = 0.0;
+    int64_t n = 0;
+    if (idx->events) {
+        for (auto& e : *idx->events) {
+            float a = 0.f, c = 0.f;
+            PQ_CUDA(cudaEventSynchronize(e.c));
+            PQ_CUDA(cudaEventElapsedTime(&a, e.a, e.b));
+            PQ_CUDA(cudaEventElapsedTime(&c, e.b, e.c));
+            t2 += a; t3 += c; ++n;
+            cudaEventDestroy(e.a); cudaEventDestroy(e.b); cudaEventDestroy(e.c);
+        }
+        idx->events->clear();
+    }
+    if (k2_ms) *k2_ms = t2;
+    if (k3_ms) *k3_ms = t3;
+    if (launches) *launches = n;
+    PQ_API_END
+}
+
+}  // extern "C"

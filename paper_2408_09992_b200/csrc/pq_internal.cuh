@@ -1,0 +1,136 @@
+// pq_internal.cuh — internals shared by the libpqtopk translation units.
+// (Product path only; the CPU oracle under oracle/ shares nothing with this.)
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stddef.h>
+#include <string>
+#include <atomic>
+#include <algorithm>
+#include <vector>
+
+#include "../../include/pqtopk.h"
+
+namespace pq {
+
+// ----------------------------------------------------------------------------
+// Error plumbing: every ABI entry point catches and converts to pq_status.
+// ----------------------------------------------------------------------------
+struct Error {
+    pq_status st;
+    std::string msg;
+};
+void set_error(const std::string& msg);
+void clear_error();
+[[noreturn]] void fail(pq_status st, const std::string& msg);
+void check_cuda(cudaError_t e, const char* what);
+void check_launch(const char* what);        // cudaGetLastError after a launch
+extern std::atomic<int64_t> g_launches;     // kernels launched by this library
+inline void count_launch(int n = 1) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+#define PQ_CUDA(x) ::pq::check_cuda((x), #x)
+
+// ----------------------------------------------------------------------------
+// Ranking key (reading R3): 64-bit unsigned, larger = ranks earlier.
+//   high 32 bits: order-preserving image of the fp32 score bits
+//   low  32 bits: 0xFFFFFFFF - global id   (smaller id ranks earlier on ties)
+// Key 0 is never produced by a real (score, id) pair and marks "empty".
+// ----------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t make_key(float s, uint32_t gid) {
+    uint32_t u = __float_as_uint(s);
+    uint32_t o = (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+    return ((uint64_t)o << 32) | (uint64_t)(0xFFFFFFFFu - gid);
+}
+__device__ __forceinline__ float key_score(uint64_t k) {
+    uint32_t o = (uint32_t)(k >> 32);
+    uint32_t u = (o & 0x80000000u) ? (o & 0x7FFFFFFFu) : ~o;
+    return __uint_as_float(u);
+}
+__device__ __forceinline__ int32_t key_id(uint64_t k) {
+    return (int32_t)(0xFFFFFFFFu - (uint32_t)k);
+}
+
+// ----------------------------------------------------------------------------
+// Index
+// ----------------------------------------------------------------------------
+struct Layout {
+    int32_t mp;            // bytes per item row in d_codes (m rounded up to 4)
+    int32_t paired;        // 1: rows are in pair order (see k0), d_perm valid
+};
+
+}  // namespace pq
+
+struct pq_index_s {
+    int64_t N = 0;
+    int32_t m = 0, b = 0;
+    int64_t id_base = 0;
+    int device = 0;
+    int num_sms = 0;
+    size_t smem_optin = 0;
+    pq::Layout lay{};
+    uint8_t* d_codes = nullptr;    // [N_rows][mp] internal code rows (+ tail pad)
+    int32_t* d_perm = nullptr;     // row -> local item id (only if lay.paired)
+    uint8_t* d_cmap = nullptr;     // [m][b] stored code -> original code (paired)
+    int64_t n_rows = 0;            // rows in d_codes (>= N when paired, padded)
+    pq_tuning tuning{};
+    // optional K2/K3 timing (pq_timing_enable)
+    int timing = 0;
+    struct EvTriple { cudaEvent_t a, b, c; };
+    std::vector<EvTriple>* events = nullptr;
+};
+
+namespace pq {
+
+// ---- kernels / launchers implemented in the .cu files ----------------------
+// K0 (k0_relayout.cu)
+void launch_relayout(const uint8_t* src, int64_t N, int m, int b, uint8_t* dst, int mp,
+                     unsigned long long* first_bad, cudaStream_t st);
+
+// K1 (k1_subscores.cu)
+void launch_subscores(const float* phi, const float* psi, int B, int d, int m, int b,
+                      float* S, cudaStream_t st);
+
+// K2 (k2_score_select.cu)
+struct K2Plan {
+    int G = 0, Ug = 0, W = 0, J = 0, cap = 0;
+    int n_groups = 0, chunks = 0, grid = 0;
+    int64_t chunk_items = 0;
+    size_t smem = 0;
+    size_t lanebuf_bytes = 0;     // grid * W * 32 * cap * 8
+    size_t cand_bytes = 0;        // B * chunks * K * 8
+    int variant = 1;
+};
+K2Plan plan_k2(const pq_index_s* idx, int B, int K);
+void launch_k2(const pq_index_s* idx, const K2Plan& p, const float* S, int B, int K,
+               uint64_t* lanebuf, uint64_t* cand, cudaStream_t st);
+
+// K3 (k3_select.cu): segmented exact top-K
+constexpr int K3_SEG = 16384;          // keys per K3 block (smem-resident)
+size_t k3_reduce_scratch_bytes(int64_t L, int B, int K);
+// keys [B][L] -> ids/scores [B][K] (sorted), multi-level; scratch from above
+void k3_keys_to_topk(const uint64_t* keys, int64_t L, int B, int K, void* scratch,
+                     int32_t* ids, float* scores, cudaStream_t st);
+// pairs [P][B][K] -> ids/scores [B][K]
+size_t k3_pairs_scratch_bytes(int P, int B, int K);
+void k3_pairs_to_topk(const int32_t* ids_in, const float* sc_in, int P, int B, int K,
+                      void* scratch, int32_t* ids, float* scores, cudaStream_t st);
+// score rows R[B][ld] (cols [0,n)) -> keys appended at out[u][list_off .. ) in
+// lists of K; returns the number of lists written per user
+int k3_rows_lists(int64_t n);
+void k3_rows_to_keys(const float* R, int64_t ld, int64_t n, int B, int K, uint32_t id0,
+                     uint64_t* out, int64_t out_lists_per_user, int64_t list_off,
+                     cudaStream_t st);
+
+// K4 (k4_dense.cu)
+void launch_reconstruct(const pq_index_s* idx, const float* psi, int d, float* W,
+                        cudaStream_t st);
+void dense_sgemm(const float* W, int64_t Nc, int d, const float* phi, int B, float* R,
+                 cudaStream_t st);
+void launch_recjpq_split(const pq_index_s* idx, const float* S, int B, int u0, int Bc,
+                         int k, float* R, cudaStream_t st);
+
+__host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+__host__ __device__ inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+}  // namespace pq

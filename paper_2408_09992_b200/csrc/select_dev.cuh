@@ -1,0 +1,105 @@
+// select_dev.cuh — device helpers for exact top-K selection on 64-bit keys
+// (K2 lane-buffer flushes, K2 CTA merge, K3).  Radix select, 8 bits per pass,
+// most significant digit first; keys are unique except the empty key 0.
+#pragma once
+#include "pq_internal.cuh"
+
+namespace pq {
+
+constexpr unsigned FULL = 0xFFFFFFFFu;
+
+__device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31; }
+__device__ __forceinline__ unsigned lanemask_lt() {
+    unsigned r;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(r));
+    return r;
+}
+
+// Warp-aggregated histogram increment; all 32 lanes must call it.
+__device__ __forceinline__ void hist_add(uint32_t* hist, bool ok, uint32_t digit) {
+    unsigned d = ok ? digit : 0xFFFFFFFFu;
+    unsigned peers = __match_any_sync(FULL, d);
+    if (ok && lane_id() == (unsigned)(__ffs(peers) - 1)) atomicAdd(&hist[digit], __popc(peers));
+}
+
+// One full warp: given a 256-bin histogram of the keys that match the current
+// prefix and krem >= 1 keys still to take (krem <= total), find the digit d*
+// holding the krem-th largest key and the count of keys in higher bins.
+__device__ __forceinline__ void warp_find_digit(const uint32_t* hist, uint32_t krem,
+                                                uint32_t& digit, uint32_t& above_out) {
+    const int lane = lane_id();
+    const int base = 8 * (31 - lane);          // lane 0 owns the top bins
+    uint32_t c[8], local = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) { c[j] = hist[base + j]; local += c[j]; }
+    uint32_t incl = local;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        uint32_t v = __shfl_up_sync(FULL, incl, off);
+        if (lane >= off) incl += v;
+    }
+    uint32_t run = incl - local;               // keys in bins above my range
+    int found = -1;
+    uint32_t gt = 0;
+#pragma unroll
+    for (int j = 7; j >= 0; --j) {
+        if (found < 0 && run < krem && run + c[j] >= krem) { found = base + j; gt = run; }
+        run += c[j];
+    }
+    unsigned bm = __ballot_sync(FULL, found >= 0);
+    int src = bm ? __ffs(bm) - 1 : 0;
+    digit = (uint32_t)__shfl_sync(FULL, found, src);
+    above_out = __shfl_sync(FULL, gt, src);
+}
+
+// Warp-level: the K-th largest of keys buf[0..n) (global or shared), n >= K >= 1.
+// hist: 256 words of shared memory private to this warp.
+__device__ __forceinline__ uint64_t warp_kth(const uint64_t* buf, int n, uint32_t K,
+                                             uint32_t* hist) {
+    uint64_t prefix = 0;
+    uint32_t krem = K;
+    const int lane = lane_id();
+    for (int shift = 56; shift >= 0; shift -= 8) {
+        const uint64_t hmask = (shift == 56) ? 0ull : (~0ull << (shift + 8));
+#pragma unroll
+        for (int i = lane; i < 256; i += 32) hist[i] = 0;
+        __syncwarp();
+        for (int i0 = 0; i0 < n; i0 += 32) {
+            int i = i0 + lane;
+            uint64_t v = i < n ? buf[i] : 0ull;
+            bool ok = (i < n) && ((v & hmask) == prefix);
+            hist_add(hist, ok, (uint32_t)(v >> shift) & 255u);
+        }
+        __syncwarp();
+        uint32_t dg, ab;
+        warp_find_digit(hist, krem, dg, ab);
+        prefix |= (uint64_t)dg << shift;
+        krem -= ab;
+        __syncwarp();
+    }
+    return prefix;
+}
+
+// Block-level bitonic sort (descending) of s[0..n), n a power of two.
+__device__ __forceinline__ void block_bitonic_desc(uint64_t* s, int n) {
+    for (int size = 2; size <= n; size <<= 1) {
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            for (int i = threadIdx.x; i < (n >> 1); i += blockDim.x) {
+                int lo = 2 * stride * (i / stride) + (i % stride);
+                int hi = lo + stride;
+                bool desc = (lo & size) == 0;
+                uint64_t a = s[lo], c = s[hi];
+                if ((a < c) == desc) { s[lo] = c; s[hi] = a; }
+            }
+            __syncthreads();
+        }
+    }
+}
+
+__host__ __device__ __forceinline__ int pow2_ceil(int x) {
+    int p = 1;
+    while (p < x) p <<= 1;
+    return p;
+}
+
+}  // namespace pq
