@@ -8,9 +8,10 @@
 // Layout ("row groups", variant 1).  A CTA owns Ug users (a user group) and a
 // contiguous item chunk.  Shared memory holds the users' sub-id score tables
 // interleaved by user: row (k, g) is G consecutive fp32 words, word w holding
-// S[user(w % Ug)][k][g].  Lane l of a warp serves row word l % G and item slot
-// l / G, so the P = 32/G slots of a warp look up P different items in the same
-// split: one LDS per lane per split.  G = 32 makes every warp access
+// S[user(w % Ug)][k][g] (Ug < G: the G/Ug copies are replicas).  Lane l of a
+// warp reads row word l % G and takes item slot l / Ug, so the P = 32/Ug slots
+// of a warp look up P different items in the same split: one LDS per lane per
+// split.  G = 32 makes every warp access
 // bank-conflict free (32 distinct users, one row); smaller G trades conflicts
 // for capacity (m*b*G*4 bytes must fit in shared memory; SURVEY §7 hard part 1).
 //
@@ -93,10 +94,13 @@ __global__ void __launch_bounds__(512, 1) k2_score_select(const K2Args a) {
     int* cnts = reinterpret_cast<int*>(tau_sh + 32);
     uint32_t* sh = reinterpret_cast<uint32_t*>(cnts + W * 32);
 
-    constexpr int P = 32 / G;
-    const int slot = lane / G;
-    const int lw = lane % G;
+    // Lane l reads row word l % G (user l % Ug, since Ug | G) and takes item
+    // slot l / Ug: lanes of the same user (replicas when Ug < G) get distinct
+    // items, lanes of distinct users share one item.
     const int Ug = a.Ug;
+    const int P = 32 / Ug;
+    const int slot = lane / Ug;
+    const int lw = lane % G;
     const int my_u = lane & (Ug - 1);
     uint64_t* wbuf = a.lanebuf + ((int64_t)blockIdx.x * W + warp) * 32 * a.cap;
     uint64_t* mybuf = wbuf + (int64_t)lane * a.cap;
