@@ -223,6 +223,10 @@ def run_ours(args):
     idx = pq.pq_create(codes, b=b, id_base=lo)
     torch.cuda.synchronize()
     create_s = time.perf_counter() - t0
+    if args.variant:
+        idx.set_tuning(variant=args.variant)
+    plan = idx.plan(B, K)
+    layout = idx.layout()
 
     F_d = torch.from_numpy(F).to(dev)
     P_d = torch.from_numpy(P).to(dev)
@@ -364,6 +368,7 @@ def run_ours(args):
         "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic (pqsynth, seeded; BASELINE.json config recipe)",
         "config": {"workload": workload_name(cfg), "items_per_gpu": n_local,
+                   "k2_plan": plan, "layout": layout,
                    "parallelism": f"item-shard x{world}" if world > 1 else "single GPU",
                    "l2": "256 MiB L2 flush before every timed step (outside events)"},
         "queries_per_s": B / (ms_per_step / 1e3),
@@ -392,6 +397,7 @@ def main():
     ap.add_argument("--config", default="c4", choices=sorted(pqsynth.CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--variant", type=int, default=0, help="force K2 variant (1 or 2; 0 = auto)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("bench.py: --warmup must be >= 3", file=sys.stderr)

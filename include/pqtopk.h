@@ -105,6 +105,25 @@ pq_status pq_destroy(pq_index idx);
 pq_status pq_index_info(pq_index idx, int64_t* N, int32_t* m, int32_t* b,
                         int64_t* id_base);
 
+/*
+ * Layout of an index (diagnostics; any output may be NULL):
+ *   paired      : 1 if the paired-half-warp layout (K2 v2) was built
+ *   tmem_splits : splits of that layout served from tensor memory (0 or 2)
+ *   pairs_matched / leftover_items : complementary pairs found / items paired
+ *                 without a complement (they are scored correctly but may hit
+ *                 shared-memory bank conflicts)
+ */
+pq_status pq_index_layout(pq_index idx, int32_t* paired, int32_t* tmem_splits,
+                          int64_t* pairs_matched, int64_t* leftover_items);
+
+/*
+ * The launch plan pq_score_topk would use for (B, K) (diagnostics):
+ * out[0] variant (1 row groups, 2 paired half-warps), out[1] users per table row
+ * (G), out[2] users per group, out[3] warps per CTA, out[4] CTAs, out[5] item
+ * chunks, out[6] TMEM splits, out[7] dynamic shared memory bytes.
+ */
+pq_status pq_plan_info(pq_index idx, int32_t B, int32_t K, int64_t out[8]);
+
 /* Set launch tuning for later calls on this index (not thread-safe with
  * concurrent scoring calls on the same index). NULL restores automatic. */
 pq_status pq_set_tuning(pq_index idx, const pq_tuning* t);

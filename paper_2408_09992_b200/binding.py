@@ -25,7 +25,7 @@ PQ_STATUS = {0: "PQ_OK", 1: "PQ_ERR_INVALID_ARG", 2: "PQ_ERR_CODE_RANGE", 3: "PQ
 MAX_K = 4096
 
 EXPORTS = ["pq_abi_version", "pq_last_error", "pq_launch_count", "pq_create", "pq_destroy",
-           "pq_index_info", "pq_set_tuning", "pq_subscores", "pq_topk_workspace_bytes",
+           "pq_index_info", "pq_index_layout", "pq_plan_info", "pq_set_tuning", "pq_subscores", "pq_topk_workspace_bytes",
            "pq_score_topk", "pq_search_workspace_bytes", "pq_search", "pq_merge_workspace_bytes",
            "pq_merge_topk", "pq_reconstruct", "pq_dense_workspace_bytes", "pq_dense_topk",
            "pq_recjpq_workspace_bytes", "pq_recjpq_topk", "pq_timing_enable", "pq_timing_read"]
@@ -68,6 +68,9 @@ def load_library():
         "pq_index_info": (st, [P, ctypes.POINTER(I64), ctypes.POINTER(I32), ctypes.POINTER(I32),
                                ctypes.POINTER(I64)]),
         "pq_set_tuning": (st, [P, ctypes.POINTER(Tuning)]),
+        "pq_plan_info": (st, [P, I32, I32, ctypes.POINTER(I64)]),
+        "pq_index_layout": (st, [P, ctypes.POINTER(I32), ctypes.POINTER(I32), ctypes.POINTER(I64),
+                                 ctypes.POINTER(I64)]),
         "pq_subscores": (st, [P, P, I32, I32, I32, I32, P, P]),
         "pq_topk_workspace_bytes": (SZ, [P, I32, I32]),
         "pq_score_topk": (st, [P, P, I32, I32, P, SZ, P, P, P]),
@@ -173,6 +176,22 @@ class PQIndex:
         N, m, b, ib = ctypes.c_int64(), ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int64()
         _check(L.pq_index_info(self._h, ctypes.byref(N), ctypes.byref(m), ctypes.byref(b), ctypes.byref(ib)))
         return N.value, m.value, b.value, ib.value
+
+    def layout(self):
+        """dict(paired, tmem_splits, pairs_matched, leftover_items)."""
+        p, t, mp, lo = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int64(), ctypes.c_int64()
+        _check(load_library().pq_index_layout(self._h, ctypes.byref(p), ctypes.byref(t), ctypes.byref(mp),
+                                              ctypes.byref(lo)))
+        return {"paired": p.value, "tmem_splits": t.value, "pairs_matched": mp.value,
+                "leftover_items": lo.value}
+
+    def plan(self, B: int, K: int):
+        """The K2 launch plan for (B, K) as a dict (diagnostics)."""
+        out = (ctypes.c_int64 * 8)()
+        _check(load_library().pq_plan_info(self._h, B, K, out))
+        keys = ["variant", "users_per_row", "users_per_group", "warps", "ctas", "chunks",
+                "tmem_splits", "smem_bytes"]
+        return dict(zip(keys, [int(x) for x in out]))
 
     def set_tuning(self, variant=0, ctas=0, warps=0, chunks=0, users_per_row=0):
         t = Tuning(variant, ctas, warps, chunks, users_per_row)

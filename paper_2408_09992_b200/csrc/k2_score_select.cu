@@ -24,58 +24,9 @@
 // Dropping a key below a proved threshold is safe: >= K larger keys exist.
 // At the end of a unit every lane shrinks to <= K keys and the CTA merges the
 // lanes of each user into one list of K keys (the unit's exact top-K) for K3.
-#include "select_dev.cuh"
+#include "k2_common.cuh"
 
 namespace pq {
-
-struct K2Args {
-    const uint8_t* codes;      // [rows][mp]
-    const int32_t* perm;       // row -> local id (nullable)
-    const float* S;            // [B][m][b]
-    int64_t N;                 // rows to score
-    int m, b, mp;
-    int B, K;
-    uint32_t id_base;
-    int Ug, n_groups, chunks;
-    int64_t chunk_items;
-    uint64_t* lanebuf;         // [grid][W][32][cap]
-    int cap;
-    uint64_t* cand;            // [B][chunks][K]
-};
-
-// Shrinks every lane buffer holding more than `trigger` keys to its K best and
-// raises the lane's threshold.  All 32 lanes call it.
-__device__ __forceinline__ void warp_flush(uint64_t* wbuf, int cap, int& cnt, uint64_t& tau,
-                                           float& tau_f, int K, int trigger, uint32_t* hist,
-                                           unsigned long long* tau_user) {
-    __syncwarp();
-    unsigned need = __ballot_sync(FULL, cnt > trigger);
-    const int lane = lane_id();
-    while (need) {
-        const int L = __ffs(need) - 1;
-        need &= need - 1;
-        const int n = __shfl_sync(FULL, cnt, L);
-        uint64_t* buf = wbuf + (int64_t)L * cap;
-        const uint64_t kth = warp_kth(buf, n, (uint32_t)K, hist);
-        int pos = 0;
-        for (int i0 = 0; i0 < n; i0 += 32) {
-            int i = i0 + lane;
-            uint64_t v = i < n ? buf[i] : 0ull;
-            bool keep = (i < n) && (v >= kth);
-            unsigned bm = __ballot_sync(FULL, keep);
-            __syncwarp();
-            if (keep) buf[pos + __popc(bm & lanemask_lt())] = v;
-            pos += __popc(bm);
-            __syncwarp();
-        }
-        if (lane == L) {
-            cnt = pos;                       // == K (keys are unique)
-            if (kth > tau) { tau = kth; tau_f = key_score(kth); }
-            atomicMax(tau_user, (unsigned long long)kth);
-        }
-    }
-    __syncwarp();
-}
 
 template <int G, int M, int J>
 __global__ void __launch_bounds__(512, 1) k2_score_select(const K2Args a) {
@@ -91,8 +42,8 @@ __global__ void __launch_bounds__(512, 1) k2_score_select(const K2Args a) {
     uint32_t* hist_all = reinterpret_cast<uint32_t*>(sm_raw + align_up(tbl_words * 4, 16));
     uint32_t* hist = hist_all + warp * 256;
     unsigned long long* tau_sh = reinterpret_cast<unsigned long long*>(hist_all + W * 256);
-    int* cnts = reinterpret_cast<int*>(tau_sh + 32);
-    uint32_t* sh = reinterpret_cast<uint32_t*>(cnts + W * 32);
+    int* ucnt = reinterpret_cast<int*>(tau_sh + 32);
+    int* ucur = ucnt + 32;
 
     // Lane l reads row word l % G (user l % Ug, since Ug | G) and takes item
     // slot l / Ug: lanes of the same user (replicas when Ug < G) get distinct
@@ -108,8 +59,9 @@ __global__ void __launch_bounds__(512, 1) k2_score_select(const K2Args a) {
     const int64_t units = (int64_t)a.n_groups * a.chunks;
 
     for (int64_t unit = blockIdx.x; unit < units; unit += gridDim.x) {
-        const int grp = (int)(unit / a.chunks);
-        const int chunk = (int)(unit - (int64_t)grp * a.chunks);
+        // chunk-major: concurrently running CTAs read the same code chunk (L2 reuse)
+        const int chunk = (int)(unit / a.n_groups);
+        const int grp = (int)(unit - (int64_t)chunk * a.n_groups);
         const int64_t i0 = (int64_t)chunk * a.chunk_items;
         const int64_t i1 = min(a.N, i0 + a.chunk_items);
 
@@ -120,7 +72,7 @@ __global__ void __launch_bounds__(512, 1) k2_score_select(const K2Args a) {
             const int user = grp * Ug + (w & (Ug - 1));
             T[x] = user < a.B ? a.S[(int64_t)user * m * b + row] : 0.0f;
         }
-        if (threadIdx.x < 32) tau_sh[threadIdx.x] = 0ull;
+        if (threadIdx.x < 32) { tau_sh[threadIdx.x] = 0ull; ucnt[threadIdx.x] = 0; ucur[threadIdx.x] = 0; }
         __syncthreads();
 
         const int user = grp * Ug + my_u;
@@ -209,70 +161,9 @@ __global__ void __launch_bounds__(512, 1) k2_score_select(const K2Args a) {
         // ---- end of unit: every lane to <= K keys, then per-user CTA merge --
         if (__any_sync(FULL, cnt > a.K))
             warp_flush(wbuf, a.cap, cnt, tau, tau_f, a.K, a.K, hist, &tau_sh[my_u]);
-        cnts[warp * 32 + lane] = active ? cnt : 0;
         __syncthreads();
-
-        const int lists_per_warp = 32 / Ug;          // lanes of one user in a warp
-        uint32_t* bh = hist_all;                      // block histogram (warp 0's)
-        for (int uu = 0; uu < Ug; ++uu) {
-            const int gu = grp * Ug + uu;
-            if (gu >= a.B) break;
-            const int nl = W * lists_per_warp;       // lists of this user
-            // total candidates of this user
-            if (threadIdx.x == 0) {
-                int tot = 0;
-                for (int q = 0; q < nl; ++q) tot += cnts[(q / lists_per_warp) * 32 + (q % lists_per_warp) * Ug + uu];
-                sh[3] = (uint32_t)tot;
-                sh[2] = 0;
-            }
-            __syncthreads();
-            const int tot = (int)sh[3];
-            uint64_t kth = 0;
-            if (tot > a.K) {
-                uint64_t prefix = 0;
-                uint32_t krem = (uint32_t)a.K;
-                for (int shift = 56; shift >= 0; shift -= 8) {
-                    const uint64_t hmask = (shift == 56) ? 0ull : (~0ull << (shift + 8));
-                    for (int i = threadIdx.x; i < 256; i += blockDim.x) bh[i] = 0;
-                    __syncthreads();
-                    for (int q = warp; q < nl; q += W) {
-                        const int ql = (q / lists_per_warp) * 32 + (q % lists_per_warp) * Ug + uu;
-                        const int n = cnts[ql];
-                        const uint64_t* lb = a.lanebuf + ((int64_t)blockIdx.x * W * 32 + ql) * a.cap;
-                        for (int e0 = 0; e0 < n; e0 += 32) {
-                            const int e = e0 + lane;
-                            const uint64_t v = e < n ? lb[e] : 0ull;
-                            const bool ok = (e < n) && ((v & hmask) == prefix);
-                            hist_add(bh, ok, (uint32_t)(v >> shift) & 255u);
-                        }
-                    }
-                    __syncthreads();
-                    if (warp == 0) {
-                        uint32_t dg, ab;
-                        warp_find_digit(bh, krem, dg, ab);
-                        if (lane == 0) { sh[0] = dg; sh[1] = ab; }
-                    }
-                    __syncthreads();
-                    prefix |= (uint64_t)sh[0] << shift;
-                    krem -= sh[1];
-                    __syncthreads();
-                }
-                kth = prefix;
-            }
-            uint64_t* out = a.cand + ((int64_t)gu * a.chunks + chunk) * a.K;
-            for (int q = warp; q < nl; q += W) {
-                const int ql = (q / lists_per_warp) * 32 + (q % lists_per_warp) * Ug + uu;
-                const int n = cnts[ql];
-                const uint64_t* lb = a.lanebuf + ((int64_t)blockIdx.x * W * 32 + ql) * a.cap;
-                for (int e = lane; e < n; e += 32) {
-                    const uint64_t v = lb[e];
-                    if (v >= kth) out[atomicAdd(&sh[2], 1u)] = v;
-                }
-            }
-            __syncthreads();
-            for (int j = (int)sh[2] + threadIdx.x; j < a.K; j += blockDim.x) out[j] = 0ull;
-            __syncthreads();
-        }
+        cta_merge(a, mybuf, cnt, active, my_u, Ug, grp, chunk, tau_sh, ucnt, ucur,
+                  a.mscr + (int64_t)blockIdx.x * 32 * W * a.K, (32 / Ug) * W * a.K, hist);
     }
 }
 
@@ -302,10 +193,69 @@ static K2Fn pick(int G, int m) {
 }
 
 static size_t k2_smem(int m, int b, int G, int W) {
-    return align_up((size_t)m * b * G * 4, 16) + (size_t)W * 256 * 4 + 32 * 8 + (size_t)W * 32 * 4 + 16;
+    return align_up((size_t)m * b * G * 4, 16) + (size_t)W * 256 * 4 + 32 * 8 + 64 * 4;
+}
+
+K2Fn k2_paired_fn(int m, int tm, int b);
+
+static int choose_chunks(int64_t n_items, int n_groups, int grid_full, int64_t min_items) {
+    const int64_t max_c = std::max<int64_t>(1, std::min<int64_t>(4096, n_items / min_items));
+    int best = 1;
+    double best_eff = -1.0;
+    for (int64_t c = 1; c <= max_c; ++c) {
+        int64_t units = (int64_t)n_groups * c;
+        int64_t waves = ceil_div(units, grid_full);
+        double eff = (double)units / (double)(waves * grid_full);
+        if (eff > best_eff + 1e-9) { best_eff = eff; best = (int)c; }
+        if (eff >= 0.97) break;
+    }
+    return best;
+}
+
+static K2Plan plan_k2_paired(const pq_index_s* idx, int B, int K) {
+    K2Plan p;
+    const pq_tuning& t = idx->tuning;
+    p.variant = 2;
+    p.tm = idx->v2_tm;
+    p.W = k2_paired_warps(idx->m, p.tm, idx->b);
+    p.J = 4;
+    const int D = k2_paired_depth(idx->m, p.tm, idx->b);
+    p.G = 16;
+    p.Ug = 16;
+    p.n_groups = (int)ceil_div(B, 16);
+    p.cap = (int)align_up((size_t)std::max(2 * K, K + 4 * p.J), 32);
+    p.smem = k2_paired_smem(idx->m, p.tm, idx->b, p.W);
+    K2Fn fn = k2_paired_fn(idx->m, p.tm, idx->b);
+    PQ_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem));
+    int occ = 0;
+    PQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, p.W * 32, p.smem));
+    if (occ < 1) fail(PQ_ERR_UNSUPPORTED, "paired scoring kernel cannot be resident");
+    if (p.tm > 0) occ = 1;                      // one TMEM allocation of 512 columns per SM
+    const size_t per_cta = (size_t)p.W * 32 * p.cap * 8 + (size_t)32 * p.W * K * 8;
+    const int occ_mem = (int)std::max<size_t>(1, ((size_t)2 << 30) / (per_cta * idx->num_sms));
+    occ = std::min(occ, occ_mem);
+    const int grid_full = idx->num_sms * occ;
+    const int64_t npairs = idx->v2_rows / 2;
+    p.chunks = t.chunks > 0 ? t.chunks : choose_chunks(npairs, p.n_groups, grid_full, 1 << 14);
+    // whole CTA steps per unit (no loop tail); the overhang reads padding rows
+    const int64_t quantum = (int64_t)p.W * p.J * D;
+    p.chunk_items = (int64_t)align_up((size_t)ceil_div(npairs, p.chunks), (size_t)quantum);
+    p.chunks = (int)ceil_div(npairs, p.chunk_items);
+    if ((int64_t)p.chunks * p.chunk_items - npairs + (int64_t)D * p.W * p.J > V2_PAD_ROWS / 2)
+        fail(PQ_ERR_UNSUPPORTED, "internal: chunk overhang exceeds the padding rows");
+    const int64_t units = (int64_t)p.n_groups * p.chunks;
+    p.grid = (int)std::min<int64_t>(units, t.ctas > 0 ? t.ctas : grid_full);
+    p.lanebuf_bytes = (size_t)p.grid * p.W * 32 * p.cap * 8;
+    p.cand_bytes = (size_t)B * p.chunks * K * 8;
+    p.ghist_bytes = (size_t)p.grid * p.W * 256 * 4;
+    p.mscr_bytes = (size_t)p.grid * 32 * p.W * K * 8;
+    return p;
 }
 
 K2Plan plan_k2(const pq_index_s* idx, int B, int K) {
+    const pq_tuning& tt = idx->tuning;
+    if (idx->v2_ok && tt.variant != 1 && tt.users_per_row == 0 && (B >= 16 || tt.variant == 2))
+        return plan_k2_paired(idx, B, K);
     K2Plan p;
     const int m = idx->m, b = idx->b;
     const pq_tuning& t = idx->tuning;
@@ -328,40 +278,47 @@ K2Plan plan_k2(const pq_index_s* idx, int B, int K) {
     PQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, p.W * 32, p.smem));
     if (occ < 1) fail(PQ_ERR_UNSUPPORTED, "scoring kernel cannot be resident (occupancy 0)");
     // lane buffers: keep them under ~2 GiB
-    const size_t per_cta = (size_t)p.W * 32 * p.cap * 8;
+    const size_t per_cta = (size_t)p.W * 32 * p.cap * 8 + (size_t)32 * p.W * K * 8;
     const int occ_mem = (int)std::max<size_t>(1, ((size_t)2 << 30) / (per_cta * idx->num_sms));
     occ = std::min(occ, occ_mem);
     const int grid_full = idx->num_sms * occ;
 
     const int64_t N = idx->N;
-    if (t.chunks > 0) {
-        p.chunks = t.chunks;
-    } else {
-        const int64_t min_items = 1 << 15;
-        const int64_t max_c = std::max<int64_t>(1, std::min<int64_t>(4096, N / min_items));
-        int best = 1;
-        double best_eff = -1.0;
-        for (int64_t c = 1; c <= max_c; ++c) {
-            int64_t units = (int64_t)p.n_groups * c;
-            int64_t waves = ceil_div(units, grid_full);
-            double eff = (double)units / (double)(waves * grid_full);
-            if (eff > best_eff + 1e-9) { best_eff = eff; best = (int)c; }
-            if (eff >= 0.97) break;
-        }
-        p.chunks = best;
-    }
+    p.chunks = t.chunks > 0 ? t.chunks : choose_chunks(N, p.n_groups, grid_full, 1 << 15);
     p.chunk_items = ceil_div(N, p.chunks);
     p.chunks = (int)ceil_div(N, p.chunk_items);
     const int64_t units = (int64_t)p.n_groups * p.chunks;
     p.grid = (int)std::min<int64_t>(units, t.ctas > 0 ? t.ctas : grid_full);
     p.lanebuf_bytes = (size_t)p.grid * p.W * 32 * p.cap * 8;
     p.cand_bytes = (size_t)B * p.chunks * K * 8;
+    p.mscr_bytes = (size_t)p.grid * 32 * p.W * K * 8;
     return p;
 }
 
 void launch_k2(const pq_index_s* idx, const K2Plan& p, const float* S, int B, int K,
                uint64_t* lanebuf, uint64_t* cand, cudaStream_t st) {
-    K2Args a;
+    K2Args a{};
+    if (p.variant == 2) {
+        a.codes16 = idx->d_codes16;
+        a.perm = idx->d_perm16;
+        a.cmap = idx->d_cmap16;
+        a.pos = idx->d_pos16;
+        a.S = S;
+        a.N = idx->v2_rows;
+        a.m = idx->m; a.b = idx->b; a.mp = idx->m;
+        a.B = B; a.K = K;
+        a.id_base = (uint32_t)idx->id_base;
+        a.Ug = 16; a.n_groups = p.n_groups; a.chunks = p.chunks; a.chunk_items = p.chunk_items;
+        a.lanebuf = lanebuf; a.cap = p.cap; a.cand = cand;
+        a.tmem_splits = p.tm;
+        a.ghist = reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(lanebuf) + align_up(p.lanebuf_bytes, 256));
+        a.mscr = reinterpret_cast<uint64_t*>(reinterpret_cast<char*>(a.ghist) + align_up(p.ghist_bytes, 256));
+        K2Fn fn = k2_paired_fn(idx->m, p.tm, idx->b);
+        fn<<<p.grid, p.W * 32, p.smem, st>>>(a);
+        count_launch();
+        check_launch("k2_paired");
+        return;
+    }
     a.codes = idx->d_codes;
     a.perm = idx->lay.paired ? idx->d_perm : nullptr;
     a.S = S;
@@ -371,6 +328,8 @@ void launch_k2(const pq_index_s* idx, const K2Plan& p, const float* S, int B, in
     a.id_base = (uint32_t)idx->id_base;
     a.Ug = p.Ug; a.n_groups = p.n_groups; a.chunks = p.chunks; a.chunk_items = p.chunk_items;
     a.lanebuf = lanebuf; a.cap = p.cap; a.cand = cand;
+    a.mscr = reinterpret_cast<uint64_t*>(reinterpret_cast<char*>(lanebuf) + align_up(p.lanebuf_bytes, 256) +
+                                         align_up(p.ghist_bytes, 256));
     K2Fn fn = pick(p.G, idx->m);
     fn<<<p.grid, p.W * 32, p.smem, st>>>(a);
     count_launch();

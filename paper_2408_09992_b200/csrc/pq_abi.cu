@@ -56,7 +56,8 @@ struct TopkWs {
 static TopkWs topk_ws(const pq_index_s* idx, int B, int K) {
     TopkWs w{};
     w.plan = plan_k2(idx, B, K);
-    w.lanebuf = align_up(w.plan.lanebuf_bytes, 256);
+    w.lanebuf = align_up(w.plan.lanebuf_bytes, 256) + align_up(w.plan.ghist_bytes, 256) +
+                align_up(w.plan.mscr_bytes, 256);
     w.cand = align_up(w.plan.cand_bytes, 256);
     w.k3 = align_up(k3_reduce_scratch_bytes((int64_t)w.plan.chunks * K, B, K), 256);
     w.total = w.lanebuf + w.cand + w.k3;
@@ -69,7 +70,7 @@ static void run_score_topk(pq_index_s* idx, const float* S, int B, int K, void* 
     if (!ws || ws_bytes < w.total)
         fail(PQ_ERR_WORKSPACE, "workspace too small: need " + std::to_string(w.total) + " bytes");
     Carve c(ws);
-    uint64_t* lanebuf = c.take<uint64_t>(w.plan.lanebuf_bytes);
+    uint64_t* lanebuf = c.take<uint64_t>(w.lanebuf);     // lane buffers (+ v2 flush histograms)
     uint64_t* cand = c.take<uint64_t>(w.plan.cand_bytes);
     void* k3s = c.take<char>(k3_reduce_scratch_bytes((int64_t)w.plan.chunks * K, B, K));
     pq_index_s::EvTriple ev{};
@@ -102,6 +103,44 @@ static int64_t dense_lists(int64_t N, int64_t nc) {
     int64_t lists = 0;
     for (int64_t c0 = 0; c0 < N; c0 += nc) lists += k3_rows_lists(std::min(nc, N - c0));
     return lists;
+}
+
+// K2 v2 layout (pairing.cu) when the shape is supported: b = 256, m in {4, 8, 16},
+// 16 users' tables in shared memory, or all but two splits (+2 in TMEM).
+static void build_v2_layout(pq_index_s* idx, const uint8_t* codes_in, const uint8_t* dev_src,
+                            cudaStream_t st) {
+    const int m = idx->m, b = idx->b;
+    const size_t budget = idx->smem_optin;
+    int tm = -1;
+    if (k2_paired_supported(m, 0, b) && k2_paired_smem(m, 0, b, 8) <= budget) tm = 0;
+    else if (k2_paired_supported(m, 2, b) && k2_paired_smem(m, 2, b, 8) <= budget) tm = 2;
+    if (tm < 0) return;
+    const int64_t N = idx->N;
+    std::vector<uint8_t> hbuf;
+    const uint8_t* hc = codes_in;
+    if (is_device_ptr(codes_in)) {
+        hbuf.resize((size_t)N * m);
+        PQ_CUDA(cudaMemcpyAsync(hbuf.data(), dev_src, (size_t)N * m, cudaMemcpyDeviceToHost, st));
+        PQ_CUDA(cudaStreamSynchronize(st));
+        hc = hbuf.data();
+    }
+    PairLayout L = build_pairing(hc, N, m, b, tm);
+    const size_t cbytes = (size_t)(L.rows + V2_PAD_ROWS) * m * 2;
+    PQ_CUDA(cudaMalloc(&idx->d_codes16, cbytes));
+    PQ_CUDA(cudaMalloc(&idx->d_perm16, (size_t)L.rows * 4));
+    PQ_CUDA(cudaMalloc(&idx->d_cmap16, (size_t)m * b));
+    PQ_CUDA(cudaMalloc(&idx->d_pos16, (size_t)m * b));
+    PQ_CUDA(cudaMemcpyAsync(idx->d_pos16, L.pos.data(), (size_t)m * b, cudaMemcpyHostToDevice, st));
+    PQ_CUDA(cudaMemsetAsync(idx->d_codes16, 0, cbytes, st));
+    PQ_CUDA(cudaMemcpyAsync(idx->d_codes16, L.codes16.data(), (size_t)L.rows * m * 2, cudaMemcpyHostToDevice, st));
+    PQ_CUDA(cudaMemcpyAsync(idx->d_perm16, L.perm.data(), (size_t)L.rows * 4, cudaMemcpyHostToDevice, st));
+    PQ_CUDA(cudaMemcpyAsync(idx->d_cmap16, L.cmap.data(), (size_t)m * b, cudaMemcpyHostToDevice, st));
+    PQ_CUDA(cudaStreamSynchronize(st));
+    idx->v2_ok = 1;
+    idx->v2_tm = tm;
+    idx->v2_rows = L.rows;
+    idx->v2_matched = L.matched_pairs;
+    idx->v2_leftover = L.leftover;
 }
 
 static int recjpq_users(int64_t N, int B) {
@@ -184,6 +223,7 @@ pq_status pq_create(const uint8_t* codes, int64_t N, int32_t m, int32_t b, int64
                      (long long)(bad / m), (long long)(bad % m), (unsigned)v, b);
             fail(PQ_ERR_CODE_RANGE, msg);
         }
+        build_v2_layout(idx, codes, src, st);
         if (tmp) { cudaFree(tmp); tmp = nullptr; }
         cudaFree(d_bad);
         d_bad = nullptr;
@@ -191,6 +231,10 @@ pq_status pq_create(const uint8_t* codes, int64_t N, int32_t m, int32_t b, int64
         if (tmp) cudaFree(tmp);
         if (d_bad) cudaFree(d_bad);
         if (idx->d_codes) cudaFree(idx->d_codes);
+        if (idx->d_codes16) cudaFree(idx->d_codes16);
+        if (idx->d_perm16) cudaFree(idx->d_perm16);
+        if (idx->d_cmap16) cudaFree(idx->d_cmap16);
+        if (idx->d_pos16) cudaFree(idx->d_pos16);
         delete idx;
         throw;
     }
@@ -205,6 +249,10 @@ pq_status pq_destroy(pq_index idx) {
     if (idx->d_codes) cudaFree(idx->d_codes);
     if (idx->d_perm) cudaFree(idx->d_perm);
     if (idx->d_cmap) cudaFree(idx->d_cmap);
+    if (idx->d_codes16) cudaFree(idx->d_codes16);
+    if (idx->d_perm16) cudaFree(idx->d_perm16);
+    if (idx->d_cmap16) cudaFree(idx->d_cmap16);
+    if (idx->d_pos16) cudaFree(idx->d_pos16);
     if (idx->events) {
         for (auto& e : *idx->events) { cudaEventDestroy(e.a); cudaEventDestroy(e.b); cudaEventDestroy(e.c); }
         delete idx->events;
@@ -220,6 +268,28 @@ pq_status pq_index_info(pq_index idx, int64_t* N, int32_t* m, int32_t* b, int64_
     if (m) *m = idx->m;
     if (b) *b = idx->b;
     if (id_base) *id_base = idx->id_base;
+    PQ_API_END
+}
+
+pq_status pq_index_layout(pq_index idx, int32_t* paired, int32_t* tmem_splits,
+                          int64_t* pairs_matched, int64_t* leftover_items) {
+    PQ_API_BEGIN
+    need(idx != nullptr, "index is NULL");
+    if (paired) *paired = idx->v2_ok;
+    if (tmem_splits) *tmem_splits = idx->v2_tm;
+    if (pairs_matched) *pairs_matched = idx->v2_matched;
+    if (leftover_items) *leftover_items = idx->v2_leftover;
+    PQ_API_END
+}
+
+pq_status pq_plan_info(pq_index idx, int32_t B, int32_t K, int64_t out[8]) {
+    PQ_API_BEGIN
+    need(idx != nullptr && out != nullptr, "NULL argument");
+    check_topk_args(B, K);
+    need(B > 0 && K > 0, "B and K must be > 0");
+    K2Plan p = plan_k2(idx, B, K);
+    out[0] = p.variant; out[1] = p.G; out[2] = p.Ug; out[3] = p.W;
+    out[4] = p.grid; out[5] = p.chunks; out[6] = p.tm; out[7] = (int64_t)p.smem;
     PQ_API_END
 }
 

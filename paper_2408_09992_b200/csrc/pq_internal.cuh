@@ -59,6 +59,17 @@ struct Layout {
     int32_t paired;        // 1: rows are in pair order (see k0), d_perm valid
 };
 
+// K2 v2 catalogue layout (pairing.cu), built on the host in pq_create.
+struct PairLayout {
+    std::vector<uint16_t> codes16;   // [rows][m]
+    std::vector<int32_t> perm;       // [rows]
+    std::vector<uint8_t> cmap;       // [m][b] stored -> original
+    std::vector<uint8_t> pos;        // [m][b] original -> stored
+    int64_t rows = 0, matched_pairs = 0, leftover = 0;
+    int tm = 0;
+};
+PairLayout build_pairing(const uint8_t* codes, int64_t N, int m, int b, int tm);
+
 }  // namespace pq
 
 struct pq_index_s {
@@ -73,6 +84,14 @@ struct pq_index_s {
     int32_t* d_perm = nullptr;     // row -> local item id (only if lay.paired)
     uint8_t* d_cmap = nullptr;     // [m][b] stored code -> original code (paired)
     int64_t n_rows = 0;            // rows in d_codes (>= N when paired, padded)
+    // K2 v2 ("paired half-warps") layout; v2_ok = 0 when not eligible
+    int v2_ok = 0;
+    int v2_tm = 0;                 // splits served from TMEM (0 or 2)
+    int64_t v2_rows = 0, v2_matched = 0, v2_leftover = 0;
+    uint16_t* d_codes16 = nullptr; // [v2_rows + pad][m]
+    int32_t* d_perm16 = nullptr;   // [v2_rows]
+    uint8_t* d_cmap16 = nullptr;   // [m][b] stored -> original
+    uint8_t* d_pos16 = nullptr;    // [m][b] original -> stored
     pq_tuning tuning{};
     // optional K2/K3 timing (pq_timing_enable)
     int timing = 0;
@@ -99,8 +118,17 @@ struct K2Plan {
     size_t smem = 0;
     size_t lanebuf_bytes = 0;     // grid * W * 32 * cap * 8
     size_t cand_bytes = 0;        // B * chunks * K * 8
+    size_t ghist_bytes = 0;       // v2: grid * W * 256 * 4
+    size_t mscr_bytes = 0;        // grid * 32 * W * K * 8 (end-of-unit merge scratch)
     int variant = 1;
+    int tm = 0;
 };
+// v2 helpers (k2_paired.cu)
+size_t k2_paired_smem(int m, int tm, int b, int W);
+bool k2_paired_supported(int m, int tm, int b);
+int k2_paired_warps(int m, int tm, int b);
+int k2_paired_depth(int m, int tm, int b);
+constexpr int V2_PAD_ROWS = 1 << 16;     // zero rows after the last pair (unclamped loads)
 K2Plan plan_k2(const pq_index_s* idx, int B, int K);
 void launch_k2(const pq_index_s* idx, const K2Plan& p, const float* S, int B, int K,
                uint64_t* lanebuf, uint64_t* cand, cudaStream_t st);

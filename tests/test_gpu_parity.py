@@ -267,3 +267,38 @@ def test_invariants_and_launch_count(pq, torch, orc):
         key = [(-float(s), int(i)) for s, i in zip(sc[u], ids[u])]
         assert key == sorted(key)
         assert np.array_equal(orc.scores_numpy(G[ids[u]], S[u]).view(np.uint32), sc[u].view(np.uint32))
+
+
+@pytest.mark.parametrize("m,B,dist", [(8, 48, "uniform"), (16, 33, "uniform"), (8, 20, "zipf"), (4, 64, "few")])
+def test_paired_layout_matches_generic(pq, torch, orc, m, B, dist):
+    """K2 v2 (paired half-warps, TMEM for m=16) == K2 v1 == oracle, bit for bit;
+    and two v2 launch geometries agree."""
+    N = 1_500_001 if m == 16 else 150_001         # m = 16: 65,536 colour classes
+    G, P, F = pqsynth.random_instance(200 + m, N, m, 256, 4 * m, B, code_dist=dist)
+    idx = pq.pq_create(G, b=256, id_base=3)
+    lay = idx.layout()
+    assert lay["paired"] == 1 and lay["tmem_splits"] == (2 if m == 16 else 0)
+    if dist == "uniform":
+        assert lay["leftover_items"] < 0.2 * G.shape[0]
+    S_t = pq.pq_subscores(cuda(torch, F), cuda(torch, P))
+    K = 64
+    outs = []
+    for tun in (dict(), dict(variant=1), dict(variant=2, ctas=5, chunks=11), dict(variant=2, chunks=1)):
+        idx.set_tuning(**tun)
+        i, s = pq.pq_score_topk(idx, S_t, K)
+        outs.append((i.cpu().numpy(), s.cpu().numpy()))
+    for o in outs[1:]:
+        assert_same(*outs[0], *o)
+    assert_same(*outs[0], *orc.pq_topk(G, S_t.cpu().numpy(), K, id_base=3))
+    # dense reconstruction must use the ORIGINAL codes (cmap), not the stored ones
+    W = pq.pq_reconstruct(idx, cuda(torch, P)).cpu().numpy()
+    assert np.array_equal(W, orc.reconstruct(G, P))
+
+
+def test_paired_sparse_classes(pq, torch, orc):
+    """m = 16 with few items: most signature classes have no complement, so
+    nearly every item is a leftover (pairing must still cover every item)."""
+    G, P, F = pqsynth.random_instance(230, 20_011, 16, 256, 64, 17)
+    S, ids, sc, idx = run_pq(pq, torch, G, P, F, 50)
+    assert idx.layout()["paired"] == 1
+    assert_same(ids, sc, *orc.pq_topk(G, S, 50))
