@@ -64,7 +64,8 @@ typedef enum {
 /* Optional launch tuning (all 0 = automatic).  Any setting gives bit-identical
  * results; this exists for tests (F12: two geometries, same bits) and tuning. */
 typedef struct {
-    int32_t variant;     /* 0 auto; 1 = generic row-group kernel; 2 = paired half-warps */
+    int32_t variant;     /* 0 auto; 1 = generic row-group kernel; 2 = paired half-warps;
+                            3 = tiled phases (4 users per lane, TMA tables, TMEM partials) */
     int32_t ctas;        /* persistent CTAs of the scoring kernel (0 = #SMs x occupancy) */
     int32_t warps;       /* warps per CTA of the scoring kernel (0 = auto) */
     int32_t chunks;      /* item chunks per user group (0 = auto) */
@@ -116,9 +117,13 @@ pq_status pq_index_info(pq_index idx, int64_t* N, int32_t* m, int32_t* b,
 pq_status pq_index_layout(pq_index idx, int32_t* paired, int32_t* tmem_splits,
                           int64_t* pairs_matched, int64_t* leftover_items);
 
+/* Bit mask of the K2 scoring variants this index supports (bit v set:
+ * variant v usable; bit 1 is always set). */
+pq_status pq_index_variants(pq_index idx, int32_t* mask);
+
 /*
  * The launch plan pq_score_topk would use for (B, K) (diagnostics):
- * out[0] variant (1 row groups, 2 paired half-warps), out[1] users per table row
+ * out[0] variant (1 row groups, 2 paired half-warps, 3 tiled phases), out[1] users per table row
  * (G), out[2] users per group, out[3] warps per CTA, out[4] CTAs, out[5] item
  * chunks, out[6] TMEM splits, out[7] dynamic shared memory bytes.
  */

@@ -25,7 +25,7 @@ PQ_STATUS = {0: "PQ_OK", 1: "PQ_ERR_INVALID_ARG", 2: "PQ_ERR_CODE_RANGE", 3: "PQ
 MAX_K = 4096
 
 EXPORTS = ["pq_abi_version", "pq_last_error", "pq_launch_count", "pq_create", "pq_destroy",
-           "pq_index_info", "pq_index_layout", "pq_plan_info", "pq_set_tuning", "pq_subscores", "pq_topk_workspace_bytes",
+           "pq_index_info", "pq_index_layout", "pq_index_variants", "pq_plan_info", "pq_set_tuning", "pq_subscores", "pq_topk_workspace_bytes",
            "pq_score_topk", "pq_search_workspace_bytes", "pq_search", "pq_merge_workspace_bytes",
            "pq_merge_topk", "pq_reconstruct", "pq_dense_workspace_bytes", "pq_dense_topk",
            "pq_recjpq_workspace_bytes", "pq_recjpq_topk", "pq_timing_enable", "pq_timing_read"]
@@ -71,6 +71,7 @@ def load_library():
         "pq_plan_info": (st, [P, I32, I32, ctypes.POINTER(I64)]),
         "pq_index_layout": (st, [P, ctypes.POINTER(I32), ctypes.POINTER(I32), ctypes.POINTER(I64),
                                  ctypes.POINTER(I64)]),
+        "pq_index_variants": (st, [P, ctypes.POINTER(I32)]),
         "pq_subscores": (st, [P, P, I32, I32, I32, I32, P, P]),
         "pq_topk_workspace_bytes": (SZ, [P, I32, I32]),
         "pq_score_topk": (st, [P, P, I32, I32, P, SZ, P, P, P]),
@@ -184,6 +185,12 @@ class PQIndex:
                                               ctypes.byref(lo)))
         return {"paired": p.value, "tmem_splits": t.value, "pairs_matched": mp.value,
                 "leftover_items": lo.value}
+
+    def variants(self):
+        """Set of K2 scoring variants this index supports (1 generic, 2 paired, 3 tiled)."""
+        m = ctypes.c_int32()
+        _check(load_library().pq_index_variants(self._h, ctypes.byref(m)))
+        return {v for v in (1, 2, 3) if m.value >> v & 1}
 
     def plan(self, B: int, K: int):
         """The K2 launch plan for (B, K) as a dict (diagnostics)."""

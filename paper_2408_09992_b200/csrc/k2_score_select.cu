@@ -254,6 +254,11 @@ static K2Plan plan_k2_paired(const pq_index_s* idx, int B, int K) {
 
 K2Plan plan_k2(const pq_index_s* idx, int B, int K) {
     const pq_tuning& tt = idx->tuning;
+    if (idx->v3_ok && (tt.variant == 3 || (tt.variant == 0 && tt.users_per_row == 0 && B >= 16))) {
+        K2Plan p;
+        plan_k2_tiled(idx, B, K, p);
+        return p;
+    }
     if (idx->v2_ok && tt.variant != 1 && tt.users_per_row == 0 && (B >= 16 || tt.variant == 2))
         return plan_k2_paired(idx, B, K);
     K2Plan p;

@@ -57,7 +57,7 @@ static TopkWs topk_ws(const pq_index_s* idx, int B, int K) {
     TopkWs w{};
     w.plan = plan_k2(idx, B, K);
     w.lanebuf = align_up(w.plan.lanebuf_bytes, 256) + align_up(w.plan.ghist_bytes, 256) +
-                align_up(w.plan.mscr_bytes, 256);
+                align_up(w.plan.mscr_bytes, 256) + align_up(w.plan.st_bytes, 256);
     w.cand = align_up(w.plan.cand_bytes, 256);
     w.k3 = align_up(k3_reduce_scratch_bytes((int64_t)w.plan.chunks * K, B, K), 256);
     w.total = w.lanebuf + w.cand + w.k3;
@@ -73,12 +73,18 @@ static void run_score_topk(pq_index_s* idx, const float* S, int B, int K, void* 
     uint64_t* lanebuf = c.take<uint64_t>(w.lanebuf);     // lane buffers (+ v2 flush histograms)
     uint64_t* cand = c.take<uint64_t>(w.plan.cand_bytes);
     void* k3s = c.take<char>(k3_reduce_scratch_bytes((int64_t)w.plan.chunks * K, B, K));
+    char* lb = reinterpret_cast<char*>(lanebuf);
+    uint64_t* mscr = reinterpret_cast<uint64_t*>(lb + align_up(w.plan.lanebuf_bytes, 256));
+    float* St = reinterpret_cast<float*>(lb + align_up(w.plan.lanebuf_bytes, 256) +
+                                         align_up(w.plan.mscr_bytes, 256));
+    if (w.plan.variant == 3) launch_k2_tiled_prep(idx, w.plan, S, B, St, st);   // S -> tiled tables
     pq_index_s::EvTriple ev{};
     if (idx->timing) {
         PQ_CUDA(cudaEventCreate(&ev.a)); PQ_CUDA(cudaEventCreate(&ev.b)); PQ_CUDA(cudaEventCreate(&ev.c));
         PQ_CUDA(cudaEventRecord(ev.a, st));
     }
-    launch_k2(idx, w.plan, S, B, K, lanebuf, cand, st);
+    if (w.plan.variant == 3) launch_k2_tiled(idx, w.plan, B, K, lanebuf, mscr, St, cand, st);
+    else launch_k2(idx, w.plan, S, B, K, lanebuf, cand, st);
     if (idx->timing) PQ_CUDA(cudaEventRecord(ev.b, st));
     k3_keys_to_topk(cand, (int64_t)w.plan.chunks * K, B, K, k3s, ids, scores, st);
     if (idx->timing) {
@@ -141,6 +147,50 @@ static void build_v2_layout(pq_index_s* idx, const uint8_t* codes_in, const uint
     idx->v2_rows = L.rows;
     idx->v2_matched = L.matched_pairs;
     idx->v2_leftover = L.leftover;
+}
+
+// K2 v3 layout: the same colour pairing with every split in shared memory,
+// rows padded to whole tiles of V3_TILE_ROWS, codes phase-blocked
+// ([tile][phase][row][PS], k2_tiled.cu).
+static void build_v3_layout(pq_index_s* idx, const uint8_t* codes_in, const uint8_t* dev_src,
+                            cudaStream_t st) {
+    const int m = idx->m, b = idx->b;
+    if (!k2_tiled_supported(m, b) || k2_tiled_smem(m, b, 16) > idx->smem_optin) return;
+    const int64_t N = idx->N;
+    std::vector<uint8_t> hbuf;
+    const uint8_t* hc = codes_in;
+    if (is_device_ptr(codes_in)) {
+        hbuf.resize((size_t)N * m);
+        PQ_CUDA(cudaMemcpyAsync(hbuf.data(), dev_src, (size_t)N * m, cudaMemcpyDeviceToHost, st));
+        PQ_CUDA(cudaStreamSynchronize(st));
+        hc = hbuf.data();
+    }
+    PairLayout L = build_pairing(hc, N, m, b, 0);
+    const int64_t TR = V3_TILE_ROWS;
+    const int64_t tiles = ceil_div(L.rows, TR);
+    const int ps = k2_tiled_ps(m), np = m / ps;
+    std::vector<uint16_t> c3((size_t)tiles * TR * m, 0);
+    std::vector<int32_t> p3((size_t)tiles * TR, -1);
+    for (int64_t r = 0; r < L.rows; ++r) {
+        const int64_t t = r / TR, rr = r % TR;
+        p3[(size_t)r] = L.perm[(size_t)r];
+        for (int ph = 0; ph < np; ++ph)
+            for (int kk = 0; kk < ps; ++kk)
+                c3[(size_t)(((t * np + ph) * TR + rr) * ps + kk)] = L.codes16[(size_t)r * m + ph * ps + kk];
+    }
+    const size_t cbytes = c3.size() * 2 + V3_CODE_PAD;
+    PQ_CUDA(cudaMalloc(&idx->d_codes3, cbytes));
+    PQ_CUDA(cudaMalloc(&idx->d_perm3, p3.size() * 4));
+    PQ_CUDA(cudaMalloc(&idx->d_cmap3, (size_t)m * b));
+    PQ_CUDA(cudaMemsetAsync(idx->d_codes3, 0, cbytes, st));
+    PQ_CUDA(cudaMemcpyAsync(idx->d_codes3, c3.data(), c3.size() * 2, cudaMemcpyHostToDevice, st));
+    PQ_CUDA(cudaMemcpyAsync(idx->d_perm3, p3.data(), p3.size() * 4, cudaMemcpyHostToDevice, st));
+    PQ_CUDA(cudaMemcpyAsync(idx->d_cmap3, L.cmap.data(), (size_t)m * b, cudaMemcpyHostToDevice, st));
+    PQ_CUDA(cudaStreamSynchronize(st));
+    idx->v3_ok = 1;
+    idx->v3_tiles = tiles;
+    idx->v3_matched = L.matched_pairs;
+    idx->v3_leftover = L.leftover;
 }
 
 static int recjpq_users(int64_t N, int B) {
@@ -224,6 +274,7 @@ pq_status pq_create(const uint8_t* codes, int64_t N, int32_t m, int32_t b, int64
             fail(PQ_ERR_CODE_RANGE, msg);
         }
         build_v2_layout(idx, codes, src, st);
+        build_v3_layout(idx, codes, src, st);
         if (tmp) { cudaFree(tmp); tmp = nullptr; }
         cudaFree(d_bad);
         d_bad = nullptr;
@@ -235,6 +286,7 @@ pq_status pq_create(const uint8_t* codes, int64_t N, int32_t m, int32_t b, int64
         if (idx->d_perm16) cudaFree(idx->d_perm16);
         if (idx->d_cmap16) cudaFree(idx->d_cmap16);
         if (idx->d_pos16) cudaFree(idx->d_pos16);
+        if (idx->d_codes3) cudaFree(idx->d_codes3);
         delete idx;
         throw;
     }
@@ -253,6 +305,7 @@ pq_status pq_destroy(pq_index idx) {
     if (idx->d_perm16) cudaFree(idx->d_perm16);
     if (idx->d_cmap16) cudaFree(idx->d_cmap16);
     if (idx->d_pos16) cudaFree(idx->d_pos16);
+    if (idx->d_codes3) cudaFree(idx->d_codes3);
     if (idx->events) {
         for (auto& e : *idx->events) { cudaEventDestroy(e.a); cudaEventDestroy(e.b); cudaEventDestroy(e.c); }
         delete idx->events;
@@ -279,6 +332,13 @@ pq_status pq_index_layout(pq_index idx, int32_t* paired, int32_t* tmem_splits,
     if (tmem_splits) *tmem_splits = idx->v2_tm;
     if (pairs_matched) *pairs_matched = idx->v2_matched;
     if (leftover_items) *leftover_items = idx->v2_leftover;
+    PQ_API_END
+}
+
+pq_status pq_index_variants(pq_index idx, int32_t* mask) {
+    PQ_API_BEGIN
+    need(idx != nullptr && mask != nullptr, "NULL argument");
+    *mask = 2 | (idx->v2_ok ? 4 : 0) | (idx->v3_ok ? 8 : 0);
     PQ_API_END
 }
 

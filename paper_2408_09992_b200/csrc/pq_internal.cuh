@@ -92,6 +92,13 @@ struct pq_index_s {
     int32_t* d_perm16 = nullptr;   // [v2_rows]
     uint8_t* d_cmap16 = nullptr;   // [m][b] stored -> original
     uint8_t* d_pos16 = nullptr;    // [m][b] original -> stored
+    // K2 v3 ("tiled phases") layout; v3_ok = 0 when not eligible
+    int v3_ok = 0;
+    int64_t v3_tiles = 0;          // tiles of 4096 rows
+    int64_t v3_matched = 0, v3_leftover = 0;
+    uint16_t* d_codes3 = nullptr;  // [tiles][NP][4096][PS] pre-shifted stored codes (+ pad)
+    int32_t* d_perm3 = nullptr;    // [tiles * 4096] row -> local id (-1 = padding)
+    uint8_t* d_cmap3 = nullptr;    // [m][b] stored -> original
     pq_tuning tuning{};
     // optional K2/K3 timing (pq_timing_enable)
     int timing = 0;
@@ -122,7 +129,19 @@ struct K2Plan {
     size_t mscr_bytes = 0;        // grid * 32 * W * K * 8 (end-of-unit merge scratch)
     int variant = 1;
     int tm = 0;
+    size_t st_bytes = 0;          // v3: tiled S tables [n_groups][m][b][16] fp32
 };
+// v3 helpers (k2_tiled.cu)
+bool k2_tiled_supported(int m, int b);
+int k2_tiled_ps(int m);
+constexpr int V3_TILE_ROWS = 4096;
+constexpr int V3_CODE_PAD = 4096;     // bytes after the last tile (prefetch overhang)
+size_t k2_tiled_smem(int m, int b, int W);
+void plan_k2_tiled(const pq_index_s* idx, int B, int K, K2Plan& p);
+void launch_k2_tiled_prep(const pq_index_s* idx, const K2Plan& p, const float* S, int B, float* St,
+                          cudaStream_t st);
+void launch_k2_tiled(const pq_index_s* idx, const K2Plan& p, int B, int K,
+                     uint64_t* lanebuf, uint64_t* mscr, const float* St, uint64_t* cand, cudaStream_t st);
 // v2 helpers (k2_paired.cu)
 size_t k2_paired_smem(int m, int tm, int b, int W);
 bool k2_paired_supported(int m, int tm, int b);

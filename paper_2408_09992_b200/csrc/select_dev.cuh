@@ -53,7 +53,10 @@ __device__ __forceinline__ void warp_find_digit(const uint32_t* hist, uint32_t k
 }
 
 // Warp-level: the K-th largest of keys buf[0..n) (global or shared), n >= K >= 1.
-// hist: 256 words of shared memory private to this warp.
+// hist: 256 words of shared memory private to this warp.  MSD radix select,
+// 8 bits per pass; once the selected bin holds exactly the krem keys still to
+// take, the K-th key is the smallest key of that bin (one min-reduction pass
+// instead of the remaining digit passes).
 __device__ __forceinline__ uint64_t warp_kth(const uint64_t* buf, int n, uint32_t K,
                                              uint32_t* hist) {
     uint64_t prefix = 0;
@@ -73,9 +76,25 @@ __device__ __forceinline__ uint64_t warp_kth(const uint64_t* buf, int n, uint32_
         __syncwarp();
         uint32_t dg, ab;
         warp_find_digit(hist, krem, dg, ab);
+        const uint32_t inbin = hist[dg];
         prefix |= (uint64_t)dg << shift;
         krem -= ab;
         __syncwarp();
+        if (shift > 0 && inbin == krem) {
+            // the K-th key is the minimum of the keys carrying `prefix`
+            const uint64_t pmask = ~0ull << shift;
+            uint64_t mn = ~0ull;
+            for (int i = lane; i < n; i += 32) {
+                const uint64_t v = buf[i];
+                if ((v & pmask) == prefix && v < mn) mn = v;
+            }
+#pragma unroll
+            for (int o = 16; o; o >>= 1) {
+                const uint64_t t = __shfl_xor_sync(FULL, mn, o);
+                mn = t < mn ? t : mn;
+            }
+            return mn;
+        }
     }
     return prefix;
 }

@@ -278,12 +278,16 @@ def test_paired_layout_matches_generic(pq, torch, orc, m, B, dist):
     idx = pq.pq_create(G, b=256, id_base=3)
     lay = idx.layout()
     assert lay["paired"] == 1 and lay["tmem_splits"] == (2 if m == 16 else 0)
+    assert idx.variants() == {1, 2, 3}
     if dist == "uniform":
         assert lay["leftover_items"] < 0.2 * G.shape[0]
     S_t = pq.pq_subscores(cuda(torch, F), cuda(torch, P))
     K = 64
     outs = []
-    for tun in (dict(), dict(variant=1), dict(variant=2, ctas=5, chunks=11), dict(variant=2, chunks=1)):
+    assert idx.plan(B, K)["variant"] == 3
+    for tun in (dict(), dict(variant=1), dict(variant=2, ctas=5, chunks=11), dict(variant=2, chunks=1),
+                dict(variant=3, warps=8, ctas=5, chunks=11), dict(variant=3, chunks=1),
+                dict(variant=3, ctas=3)):
         idx.set_tuning(**tun)
         i, s = pq.pq_score_topk(idx, S_t, K)
         outs.append((i.cpu().numpy(), s.cpu().numpy()))
@@ -302,3 +306,31 @@ def test_paired_sparse_classes(pq, torch, orc):
     S, ids, sc, idx = run_pq(pq, torch, G, P, F, 50)
     assert idx.layout()["paired"] == 1
     assert_same(ids, sc, *orc.pq_topk(G, S, 50))
+
+
+TILED_CASES = [
+    # seed, N, m, B, K, dist — ragged tiles (4096 rows), padding users, many units
+    (300, 9_000, 16, 16, 10, "uniform"),
+    (301, 250_001, 16, 37, 100, "uniform"),
+    (302, 123_457, 8, 20, 64, "zipf"),
+    (303, 70_001, 4, 64, 300, "few"),
+    (304, 40_000, 8, 17, 1000, "uniform"),
+    (305, 1_000, 16, 48, 2000, "uniform"),           # K > N
+]
+
+
+@pytest.mark.parametrize("case", TILED_CASES, ids=[str(c[0]) for c in TILED_CASES])
+def test_tiled_parity(pq, torch, orc, case):
+    """K2 v3 (4 users per lane, TMA-staged phase tables, TMEM partial sums for
+    m = 16) is bit-exact against the oracle given S, in two launch geometries."""
+    seed, N, m, B, K, dist = case
+    G, P, F = pqsynth.random_instance(seed, N, m, 256, 4 * m, B, code_dist=dist)
+    idx = pq.pq_create(G, b=256, id_base=seed)
+    assert 3 in idx.variants()
+    S_t = pq.pq_subscores(cuda(torch, F), cuda(torch, P))
+    ref = orc.pq_topk(G, S_t.cpu().numpy(), K, id_base=seed)
+    for tun in (dict(variant=3), dict(variant=3, warps=8, ctas=3, chunks=5)):
+        idx.set_tuning(**tun)
+        assert idx.plan(B, K)["variant"] == 3
+        i, s = pq.pq_score_topk(idx, S_t, K)
+        assert_same(i.cpu().numpy(), s.cpu().numpy(), *ref, str(tun))
