@@ -149,13 +149,14 @@ static void build_v2_layout(pq_index_s* idx, const uint8_t* codes_in, const uint
     idx->v2_leftover = L.leftover;
 }
 
-// K2 v3 layout: the same colour pairing with every split in shared memory,
-// rows padded to whole tiles of V3_TILE_ROWS, codes phase-blocked
-// ([tile][phase][row][PS], k2_tiled.cu).
+// K2 v3 layout (k2_tiled.cu).  R = 16: the colour pairing (every split in
+// shared memory, stored codes * 64); R = 32: item order, codes * 128.  Rows are
+// padded to whole tiles and the codes phase-blocked ([tile][phase][row][PS]).
 static void build_v3_layout(pq_index_s* idx, const uint8_t* codes_in, const uint8_t* dev_src,
                             cudaStream_t st) {
     const int m = idx->m, b = idx->b;
-    if (!k2_tiled_supported(m, b) || k2_tiled_smem(m, b, 16) > idx->smem_optin) return;
+    const int R = k2_tiled_users(m, b);
+    if (!R || k2_tiled_smem(m, b, R, 16) > idx->smem_optin) return;
     const int64_t N = idx->N;
     std::vector<uint8_t> hbuf;
     const uint8_t* hc = codes_in;
@@ -165,8 +166,22 @@ static void build_v3_layout(pq_index_s* idx, const uint8_t* codes_in, const uint
         PQ_CUDA(cudaStreamSynchronize(st));
         hc = hbuf.data();
     }
-    PairLayout L = build_pairing(hc, N, m, b, 0);
-    const int64_t TR = V3_TILE_ROWS;
+    PairLayout L;
+    if (R == 16) {
+        L = build_pairing(hc, N, m, b, 0);
+    } else {
+        L.rows = N;
+        L.perm.resize((size_t)N);
+        L.codes16.resize((size_t)N * m);
+        L.cmap.resize((size_t)m * b);
+        for (int k = 0; k < m; ++k)
+            for (int g = 0; g < b; ++g) L.cmap[(size_t)k * b + g] = (uint8_t)g;
+        for (int64_t i = 0; i < N; ++i) {
+            L.perm[(size_t)i] = (int32_t)i;
+            for (int k = 0; k < m; ++k) L.codes16[(size_t)i * m + k] = (uint16_t)(hc[i * m + k] * 128u);
+        }
+    }
+    const int64_t TR = k2_tiled_rows_per_tile(R);
     const int64_t tiles = ceil_div(L.rows, TR);
     const int ps = k2_tiled_ps(m), np = m / ps;
     std::vector<uint16_t> c3((size_t)tiles * TR * m, 0);
@@ -188,6 +203,7 @@ static void build_v3_layout(pq_index_s* idx, const uint8_t* codes_in, const uint
     PQ_CUDA(cudaMemcpyAsync(idx->d_cmap3, L.cmap.data(), (size_t)m * b, cudaMemcpyHostToDevice, st));
     PQ_CUDA(cudaStreamSynchronize(st));
     idx->v3_ok = 1;
+    idx->v3_R = R;
     idx->v3_tiles = tiles;
     idx->v3_matched = L.matched_pairs;
     idx->v3_leftover = L.leftover;

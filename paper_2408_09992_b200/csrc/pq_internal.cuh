@@ -94,7 +94,8 @@ struct pq_index_s {
     uint8_t* d_pos16 = nullptr;    // [m][b] original -> stored
     // K2 v3 ("tiled phases") layout; v3_ok = 0 when not eligible
     int v3_ok = 0;
-    int64_t v3_tiles = 0;          // tiles of 4096 rows
+    int v3_R = 0;                  // users per table row (16: paired layout, 32: item order)
+    int64_t v3_tiles = 0;          // tiles of k2_tiled_rows_per_tile(v3_R) rows
     int64_t v3_matched = 0, v3_leftover = 0;
     uint16_t* d_codes3 = nullptr;  // [tiles][NP][4096][PS] pre-shifted stored codes (+ pad)
     int32_t* d_perm3 = nullptr;    // [tiles * 4096] row -> local id (-1 = padding)
@@ -133,10 +134,11 @@ struct K2Plan {
 };
 // v3 helpers (k2_tiled.cu)
 bool k2_tiled_supported(int m, int b);
+int k2_tiled_users(int m, int b);
 int k2_tiled_ps(int m);
-constexpr int V3_TILE_ROWS = 4096;
+int k2_tiled_rows_per_tile(int R);
 constexpr int V3_CODE_PAD = 4096;     // bytes after the last tile (prefetch overhang)
-size_t k2_tiled_smem(int m, int b, int W);
+size_t k2_tiled_smem(int m, int b, int R, int W);
 void plan_k2_tiled(const pq_index_s* idx, int B, int K, K2Plan& p);
 void launch_k2_tiled_prep(const pq_index_s* idx, const K2Plan& p, const float* S, int B, float* St,
                           cudaStream_t st);

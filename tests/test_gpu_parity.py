@@ -309,23 +309,27 @@ def test_paired_sparse_classes(pq, torch, orc):
 
 
 TILED_CASES = [
-    # seed, N, m, B, K, dist — ragged tiles (4096 rows), padding users, many units
-    (300, 9_000, 16, 16, 10, "uniform"),
-    (301, 250_001, 16, 37, 100, "uniform"),
-    (302, 123_457, 8, 20, 64, "zipf"),
-    (303, 70_001, 4, 64, 300, "few"),
-    (304, 40_000, 8, 17, 1000, "uniform"),
-    (305, 1_000, 16, 48, 2000, "uniform"),           # K > N
+    # seed, N, m, b, B, K, dist — ragged tiles, padding users, many units
+    (300, 9_000, 16, 256, 16, 10, "uniform"),
+    (301, 250_001, 16, 256, 37, 100, "uniform"),
+    (302, 123_457, 8, 256, 20, 64, "zipf"),
+    (303, 70_001, 4, 256, 64, 300, "few"),           # R = 32, item order
+    (304, 40_000, 8, 256, 17, 1000, "uniform"),
+    (305, 1_000, 16, 256, 48, 2000, "uniform"),      # K > N
+    (306, 300_001, 4, 16, 70, 1000, "uniform"),      # C5-like: massive exact ties, R = 32
+    (307, 90_001, 8, 16, 33, 50, "uniform"),
+    (308, 5_003, 4, 16, 40, 3000, "uniform"),        # K close to N, ties
 ]
 
 
 @pytest.mark.parametrize("case", TILED_CASES, ids=[str(c[0]) for c in TILED_CASES])
 def test_tiled_parity(pq, torch, orc, case):
-    """K2 v3 (4 users per lane, TMA-staged phase tables, TMEM partial sums for
-    m = 16) is bit-exact against the oracle given S, in two launch geometries."""
-    seed, N, m, B, K, dist = case
-    G, P, F = pqsynth.random_instance(seed, N, m, 256, 4 * m, B, code_dist=dist)
-    idx = pq.pq_create(G, b=256, id_base=seed)
+    """K2 v3 (4 users per lane, TMA-staged tables, TMEM partial sums for
+    m = 16, CTA-wide candidate buffers) is bit-exact against the oracle given
+    S, in two launch geometries."""
+    seed, N, m, b, B, K, dist = case
+    G, P, F = pqsynth.random_instance(seed, N, m, b, 4 * m, B, code_dist=dist)
+    idx = pq.pq_create(G, b=b, id_base=seed)
     assert 3 in idx.variants()
     S_t = pq.pq_subscores(cuda(torch, F), cuda(torch, P))
     ref = orc.pq_topk(G, S_t.cpu().numpy(), K, id_base=seed)
