@@ -223,8 +223,12 @@ def run_ours(args):
     idx = pq.pq_create(codes, b=b, id_base=lo)
     torch.cuda.synchronize()
     create_s = time.perf_counter() - t0
-    if args.variant:
-        idx.set_tuning(variant=args.variant)
+    if args.variant or args.tuning:
+        tun = dict(kv.split("=") for kv in args.tuning.split(",") if kv) if args.tuning else {}
+        tun = {k: int(v) for k, v in tun.items()}
+        if args.variant:
+            tun["variant"] = args.variant
+        idx.set_tuning(**tun)
     plan = idx.plan(B, K)
     layout = idx.layout()
 
@@ -397,7 +401,8 @@ def main():
     ap.add_argument("--config", default="c4", choices=sorted(pqsynth.CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--variant", type=int, default=0, help="force K2 variant (1 or 2; 0 = auto)")
+    ap.add_argument("--variant", type=int, default=0, help="force K2 variant (1, 2 or 3; 0 = auto)")
+    ap.add_argument("--tuning", default="", help="K2 launch tuning, e.g. warps=8,chunks=9 (diagnostics)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("bench.py: --warmup must be >= 3", file=sys.stderr)

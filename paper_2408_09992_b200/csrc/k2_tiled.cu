@@ -25,7 +25,7 @@
 // Phases.  When the R users' tables exceed shared memory (C4: 16 users x 16
 // splits x 256 x 64 B = 256 KB) the splits are processed in NP phases of PS
 // splits: phase tables are loaded by the TMA bulk engine (cp.async.bulk +
-// mbarrier) from a pre-tiled copy of S into a 3-slot shared-memory ring, and
+// mbarrier) from a pre-tiled copy of S into a 2-slot shared-memory ring, and
 // the running partial sums of a tile (TR items x R users) stay in TENSOR
 // MEMORY between phases (tcgen05.st / tcgen05.ld 32x32b.x4: lane = TMEM row,
 // 4 columns per slot; each warp owns 512/(W/4) columns of its lane quadrant).
@@ -49,6 +49,7 @@
 // K-th best.  Thresholds are also shared across CTAs through gtau[user]
 // (a unit may drop an item whenever K better items are known anywhere: the
 // global top-K still survives in the union of the unit lists that K3 merges).
+#include <climits>
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
@@ -67,10 +68,12 @@ struct K2TArgs {
     int n_groups, chunks;
     int64_t chunk_tiles;       // tiles per item chunk
     uint64_t* ubuf;            // [grid][R][cap] per-user candidate buffers
-    int cap;                   // >= 2K + TR + 32
+    int cap;                   // >= 2K + 2 TR + 96 (see the shrink protocol)
     uint64_t* cand;            // [B][chunks][K]
     unsigned long long* gtau;  // [n_groups * R] per-user proved thresholds (zeroed per call)
     long long* trace;          // diagnostics (PQTOPK_K2_TRACE): CTA 0 phase timeline, or null
+    int trace_stride;          // trace every trace_stride-th tile (PQTOPK_K2_TRACE_STRIDE)
+    int* dbg;                  // diagnostics (PQTOPK_K2_DEBUG): bounded spins record state here
 };
 constexpr int TRACE_PH = 256;  // traced table uses (CTA 0): [W][TRACE_PH][3] + issue [TRACE_PH]
 
@@ -131,19 +134,18 @@ __device__ __forceinline__ float tau_to_filter(uint64_t t) {
     return t ? key_score(t) : -INFINITY;
 }
 
-// Code word(s) of one row for one phase: PS 16-bit codes.
-template <int PS> struct CodeW;
-template <> struct CodeW<4> {
-    uint32_t w[2];
+// Code words of one row for one phase and TWO consecutive slots: pq_create
+// interleaves slot pairs ([slot pair][row][2][PS] inside a phase block), so a
+// lane fetches both slots' PS 16-bit codes with 16-byte loads; words
+// [e * PS/2, (e+1) * PS/2) belong to slot parity e.
+template <int PS> struct CodePair {
+    uint32_t w[PS];
     __device__ __forceinline__ void load(const char* p) {
-        const uint2 t = __ldg(reinterpret_cast<const uint2*>(p)); w[0] = t.x; w[1] = t.y;
-    }
-};
-template <> struct CodeW<8> {
-    uint32_t w[4];
-    __device__ __forceinline__ void load(const char* p) {
-        const uint4 t = __ldg(reinterpret_cast<const uint4*>(p));
-        w[0] = t.x; w[1] = t.y; w[2] = t.z; w[3] = t.w;
+#pragma unroll
+        for (int x = 0; x < PS; x += 4) {
+            const uint4 t = __ldg(reinterpret_cast<const uint4*>(p) + x / 4);
+            w[x] = t.x; w[x + 1] = t.y; w[x + 2] = t.z; w[x + 3] = t.w;
+        }
     }
 };
 __device__ __forceinline__ uint32_t hi16_add(uint32_t w, uint32_t add) {
@@ -175,20 +177,51 @@ __device__ __noinline__ uint64_t shrink_user(uint64_t* ub, int nc, int n, int K,
                                              uint64_t* dst, uint32_t* hist, const int32_t* perm,
                                              uint32_t id_base, int& n_out) {
     const int lane = threadIdx.x & 31;
-    for (int i = nc + lane; i < n; i += 32) ub[i] = raw_to_key(ub[i], perm, id_base);
+    constexpr int U = 8;                               // independent loads in flight per lane
+    for (int i0 = nc; i0 < n; i0 += 32 * U) {
+        uint64_t r[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int i = i0 + u * 32 + lane;
+            r[u] = i < n ? ub[i] : 0ull;
+        }
+        int32_t lid[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int i = i0 + u * 32 + lane;
+            lid[u] = i < n ? __ldg(&perm[(uint32_t)r[u]]) : -1;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int i = i0 + u * 32 + lane;
+            if (i < n)
+                ub[i] = lid[u] < 0 ? 0ull
+                                   : ((r[u] & 0xFFFFFFFF00000000ull) |
+                                      (uint64_t)(0xFFFFFFFFu - (id_base + (uint32_t)lid[u])));
+        }
+    }
     __syncwarp();
     const uint64_t kth = n > K ? warp_kth(ub, n, (uint32_t)K, hist) : 0ull;
     uint64_t th = kth > floor ? kth : floor;
     if (th == 0ull) th = 1ull;                                   // key 0 = padding: never kept
     int pos = 0;
-    for (int i0 = 0; i0 < n; i0 += 32) {
-        const int i = i0 + lane;
-        const uint64_t v = i < n ? ub[i] : 0ull;
-        const bool keep = (i < n) && (v >= th);
-        const unsigned bm = __ballot_sync(FULL, keep);
+    constexpr int UC = 4;
+    for (int i0 = 0; i0 < n; i0 += 32 * UC) {
+        // in-place safe: writes land at indices <= the chunk being read
+        uint64_t v[UC];
+#pragma unroll
+        for (int u = 0; u < UC; ++u) {
+            const int i = i0 + u * 32 + lane;
+            v[u] = i < n ? ub[i] : 0ull;
+        }
         __syncwarp();
-        if (keep) dst[pos + __popc(bm & lanemask_lt())] = v;
-        pos += __popc(bm);
+#pragma unroll
+        for (int u = 0; u < UC; ++u) {
+            const bool keep = v[u] >= th;                         // (0 for i >= n)
+            const unsigned bm = __ballot_sync(FULL, keep);
+            if (keep) dst[pos + __popc(bm & lanemask_lt())] = v[u];
+            pos += __popc(bm);
+        }
         __syncwarp();
     }
     n_out = pos;
@@ -201,7 +234,8 @@ __device__ __noinline__ uint64_t shrink_user(uint64_t* ub, int nc, int n, int K,
 template <int M, int PS, int BT, int R, int W, int D>
 __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
     constexpr int NP = M / PS;
-    constexpr int NB = NP > 1 ? 3 : 1;                 // table buffers (ring)
+    constexpr int NB = NP > 1 ? 2 : 1;                 // table buffers (ring; NP even -> slot = ph & 1)
+    static_assert(NP == 1 || NP % NB == 0, "ring slot must be a compile-time function of the phase");
     constexpr int LPR = R / 4;                         // lanes per row
     constexpr int RPS = 32 / LPR;                      // rows per warp slot
     constexpr int SL = 512 / W;                        // slots per warp per tile
@@ -211,7 +245,7 @@ __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
     constexpr uint32_t TBLB = (uint32_t)PS * SPLITB;   // bytes per table buffer
     constexpr int CB = PS * 2;                         // code bytes per row per phase
     static_assert(M % PS == 0, "phases");
-    static_assert(SL % D == 0, "prefetch depth");
+    static_assert(SL % D == 0 && D % 2 == 0, "prefetch depth");
     static_assert(R == 16 || R == 32, "users per row");
 
     extern __shared__ __align__(1024) unsigned char sm_raw[];
@@ -225,7 +259,9 @@ __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
     int* nconv_u = cnt_u + R;
     unsigned long long* mbar = reinterpret_cast<unsigned long long*>(nconv_u + R);
     int* done = reinterpret_cast<int*>(mbar + NB);
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + NB);
+    int* tiles_done = done + NB;                       // [W] tiles finished by each warp
+    int* sflag = tiles_done + W;                       // [2] shrink request: tile index + 1
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sflag + 2);
     const uint32_t tbl0 = smem_u32(sm_raw);
     const uint32_t bar0 = smem_u32(mbar);
 
@@ -262,6 +298,8 @@ __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (threadIdx.x < R) { tau_sh[threadIdx.x] = 0ull; cnt_u[threadIdx.x] = 0; nconv_u[threadIdx.x] = 0; }
+    if (threadIdx.x < W) tiles_done[threadIdx.x] = 0;
+    if (threadIdx.x == 0) { sflag[0] = 0; sflag[1] = 0; }
     uint32_t tmem_base = 0;
     if constexpr (NP > 1) {
         if (warp == 0) {
@@ -296,7 +334,13 @@ __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
     uint64_t* ubuf = a.ubuf + (int64_t)blockIdx.x * R * a.cap;
     int64_t gseq = 0;                                  // table uses so far (NP > 1)
     int64_t useq = 0;                                  // units done by this CTA (NP == 1)
-    const int wm = a.cap - TR;                         // shrink watermark (next tile cannot overflow)
+    // Shrink protocol (no per-tile barrier): the insert that takes a user's
+    // buffer to `wm` entries during tile T records T + 1 in sflag[T & 1]; at
+    // the end of tile T + 1 every warp (having waited until all warps finished
+    // tile T) sees the same flag and the CTA shrinks.  Between the request and
+    // the shrink at most 2 * TR more entries arrive: cap >= wm + 2 * TR.
+    const int wm = a.cap - 2 * TR - 32;
+    int64_t tseq = 0;                                  // tiles done by this CTA
 
     for (int64_t unit = blockIdx.x; unit < units; unit += gridDim.x) {
         const int chunk = (int)(unit / a.n_groups);
@@ -317,21 +361,24 @@ __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
             const int64_t tile = tile0 + t;
 #pragma unroll
             for (int ph = 0; ph < NP; ++ph) {
-                const int buf = NP > 1 ? (int)(gseq % NB) : 0;
+                const int buf = NP > 1 ? ph % NB : 0;
                 const uint32_t par = NP > 1 ? (uint32_t)((gseq / NB) & 1) : (uint32_t)(useq & 1);
-                const bool trc = a.trace && blockIdx.x == 0 && lane == 0 && gseq < TRACE_PH;
-                if (trc) a.trace[((int64_t)warp * TRACE_PH + gseq) * 3 + 0] = clock64();
+                const int64_t tix = (tseq % a.trace_stride == 0) ? (tseq / a.trace_stride) * NP + ph : TRACE_PH;
+                const bool trc = a.trace && blockIdx.x == 0 && lane == 0 && tix < TRACE_PH;
+                if (trc) a.trace[((int64_t)warp * TRACE_PH + tix) * 3 + 0] = clock64();
                 mbar_wait(bar0 + 8u * buf, par);
-                if (trc) a.trace[((int64_t)warp * TRACE_PH + gseq) * 3 + 1] = clock64();
+                if (trc) a.trace[((int64_t)warp * TRACE_PH + tix) * 3 + 1] = clock64();
                 const char* tb = reinterpret_cast<const char*>(sm_raw) + buf * TBLB;
                 const uint32_t row0 = (uint32_t)(tile * TR) + (uint32_t)(warp * SL * RPS) + (uint32_t)(lane / LPR);
+                // codes of this warp's slot pairs: [pair][row][2 slots][PS]
                 const char* cp = reinterpret_cast<const char*>(a.codes) + ((tile * NP + ph) * TR +
-                                 (int64_t)warp * SL * RPS + lane / LPR) * CB;
-                constexpr int64_t SSTR = RPS * CB;     // bytes per slot
-                CodeW<PS> cw[D];
+                                 ((int64_t)warp * SL * RPS + (lane / LPR) * 2)) * CB;
+                constexpr int64_t PSTR = 2 * RPS * CB;  // bytes per slot pair
+                constexpr int DP = D / 2;               // slot pairs per group
+                CodePair<PS> cw[DP];
 #pragma unroll
-                for (int d = 0; d < D; ++d) cw[d].load(cp + d * SSTR);
-                cp += D * SSTR;
+                for (int d = 0; d < DP; ++d) cw[d].load(cp + d * PSTR);
+                cp += DP * PSTR;
                 uint32_t tcur[4] = {0u, 0u, 0u, 0u};   // partial sums of slot s (ph > 0)
                 if (ph > 0) {
                     tm_ld_issue(tcol0, tcur);
@@ -339,17 +386,21 @@ __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
                 }
 #pragma unroll 1
                 for (int s0 = 0; s0 < SL; s0 += D) {
+                    float4 accs[D];                    // last phase: candidate sums of the group
+                    unsigned cmask = 0u;               // last phase: bit 4d+j = slot d, user 4q+j
 #pragma unroll
                     for (int d = 0; d < D; ++d) {
                         const int s = s0 + d;
                         uint32_t off[PS];              // row offsets | user-quad offset
 #pragma unroll
                         for (int kk = 0; kk < PS; ++kk) {
-                            const uint32_t w = cw[d].w[kk >> 1];
+                            const uint32_t w = cw[d >> 1].w[(d & 1) * (PS / 2) + (kk >> 1)];
                             off[kk] = (kk & 1) ? hi16_add(w, q16) : ((w & 0xFFFFu) | q16);
                         }
-                        cw[d].load(cp);                // D slots ahead (buffer is padded)
-                        cp += SSTR;
+                        if (d & 1) {                   // both slots of the pair addressed: refill
+                            cw[d >> 1].load(cp);       // DP pairs ahead (buffer is padded)
+                            cp += PSTR;
+                        }
                         float4 v[PS];
 #pragma unroll
                         for (int kk = 0; kk < PS; ++kk) v[kk] = lds128(tb + kk * SPLITB + off[kk]);
@@ -373,26 +424,35 @@ __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
                         }
                         if (ph < NP - 1) {
                             tm_st4(tcol0 + (uint32_t)s * 4u, acc);
-                            continue;
+                        } else {
+                            // last phase: branch-free candidate filter for the group
+                            accs[d] = acc;
+                            cmask |= ((acc.x >= tf[0]) ? 1u : 0u) << (4 * d);
+                            cmask |= ((acc.y >= tf[1]) ? 2u : 0u) << (4 * d);
+                            cmask |= ((acc.z >= tf[2]) ? 4u : 0u) << (4 * d);
+                            cmask |= ((acc.w >= tf[3]) ? 8u : 0u) << (4 * d);
                         }
-                        // ---- last phase: candidate filter; rare slow path = one
-                        // shared atomic + one store per candidate
-                        const bool c0 = acc.x >= tf[0], c1 = acc.y >= tf[1];
-                        const bool c2 = acc.z >= tf[2], c3 = acc.w >= tf[3];
-                        if (c0 | c1 | c2 | c3) {
-                            const uint32_t row = row0 + (uint32_t)s * RPS;
-                            const float vv[4] = {acc.x, acc.y, acc.z, acc.w};
-                            const bool cc[4] = {c0, c1, c2, c3};
+                    }
+                    if (ph == NP - 1 && cmask) {       // rare slow path: shared atomic + store
+#pragma unroll
+                        for (int d = 0; d < D; ++d) {
+                            const uint32_t row = row0 + (uint32_t)(s0 + d) * RPS;
+                            const float vv[4] = {accs[d].x, accs[d].y, accs[d].z, accs[d].w};
 #pragma unroll
                             for (int j = 0; j < 4; ++j) {
-                                if (!cc[j]) continue;
+                                if (!(cmask >> (4 * d + j) & 1u)) continue;
                                 const int u = 4 * q + j;
                                 const int p = atomicAdd(&cnt_u[u], 1);
                                 ubuf[(int64_t)u * a.cap + p] = make_raw(vv[j] + 0.0f, row);
+                                if (p == wm) {
+                                    *reinterpret_cast<volatile int*>(&sflag[tseq & 1]) = (int)(tseq + 1);
+                                    __threadfence_block();
+                                }
                             }
                         }
                     }
                 }
+                if (NP == 1 && trc) a.trace[((int64_t)warp * TRACE_PH + tix) * 3 + 2] = clock64();
                 if constexpr (NP > 1) {
                     if (ph < NP - 1) tm_wait_st();
                     // release the buffer: the last warp to finish with it loads
@@ -400,11 +460,9 @@ __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
                     __syncwarp();
                     if (lane == 0) {
                         const int old = atomicAdd(&done[buf], 1);
-                        if (trc) a.trace[((int64_t)warp * TRACE_PH + gseq) * 3 + 2] = clock64();
+                        if (trc) a.trace[((int64_t)warp * TRACE_PH + tix) * 3 + 2] = clock64();
                         if (old == W - 1) {
                             done[buf] = 0;
-                            if (a.trace && blockIdx.x == 0 && gseq + NB < TRACE_PH)
-                                a.trace[(int64_t)W * TRACE_PH * 3 + gseq + NB] = clock64();
                             int64_t u2 = unit, t2 = t;
                             int ph2 = ph;
                             for (int st = 0; st < NB; ++st) advance(u2, t2, ph2);
@@ -415,12 +473,31 @@ __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
                 }
             }
 
-            // ---- end of tile: shrink the buffers that could overflow next tile
-            __syncthreads();                           // inserts of this tile are visible
-            bool need = false;
-#pragma unroll 1
-            for (int u = 0; u < R; ++u) need |= cnt_u[u] > wm;
-            if (need) {
+            // ---- end of tile T = tseq: shrink if requested during tile T - 1
+            __syncwarp();
+            __threadfence_block();
+            if (lane == 0) *reinterpret_cast<volatile int*>(&tiles_done[warp]) = (int)(tseq + 1);
+            // wait until every warp has finished tile T - 1 (bounds the skew to one tile)
+            for (long long spins = 0;; ++spins) {
+                const int td = lane < W ? *reinterpret_cast<volatile int*>(&tiles_done[lane]) : INT_MAX;
+                if (__all_sync(FULL, td >= (int)tseq)) break;
+                __nanosleep(64);                       // back off: spinning would steal smem cycles
+                if (a.dbg && spins > (1ll << 26)) {
+                    if (lane == 0 && atomicAdd(&a.dbg[0], 1) == 0) {
+                        a.dbg[1] = blockIdx.x; a.dbg[2] = warp; a.dbg[3] = (int)tseq;
+                        a.dbg[4] = 0; a.dbg[5] = (int)unit; a.dbg[6] = (int)t; a.dbg[7] = (int)ntl;
+                        a.dbg[8] = sflag[0]; a.dbg[9] = sflag[1];
+                    }
+                    break;
+                }
+            }
+            __threadfence_block();
+            // (always after a unit's first tile: it ran with the unit's initial,
+            // usually weak, thresholds)
+            const bool need = t == 0 || (tseq > 0 &&
+                *reinterpret_cast<volatile int*>(&sflag[(tseq - 1) & 1]) == (int)tseq);
+            if (need) {                                // uniform across the CTA
+                __syncthreads();                       // every insert so far is visible
                 for (int u = warp; u < n_valid; u += W) {
                     const int n = cnt_u[u];
                     if (n <= a.K) continue;
@@ -445,6 +522,7 @@ __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
                 for (int j = 0; j < 4; ++j)
                     if (tf[j] != INFINITY) tf[j] = fmaxf(tf[j], tau_to_filter(tau_sh[4 * q + j]));
             }
+            ++tseq;
         }
 
         // ---- end of unit: each user's buffer -> the unit's top-K list -------
@@ -502,6 +580,7 @@ typedef void (*K2TFn)(const K2TArgs);
 
 template <int M, int PS, int BT, int R>
 static K2TFn tiled_fn_w(int W) {
+    if (W == 32) return k2_tiled<M, PS, BT, R, 32, 2>;
     if (W == 16) return k2_tiled<M, PS, BT, R, 16, 4>;
     return k2_tiled<M, PS, BT, R, 8, 4>;
 }
@@ -530,9 +609,9 @@ int k2_tiled_rows_per_tile(int R) { return R == 32 ? 2048 : 4096; }
 
 size_t k2_tiled_smem(int m, int b, int R, int W) {
     const int ps = k2_tiled_ps(m);
-    const int nb = (m / ps) > 1 ? 3 : 1;
+    const int nb = (m / ps) > 1 ? 2 : 1;
     return (size_t)nb * ps * b * R * 4 + (size_t)W * 1024 + (size_t)R * 8 + (size_t)R * 8 +
-           3 * 8 + 3 * 4 + 16;
+           3 * 8 + 3 * 4 + (size_t)(W + 2) * 4 + 16;
 }
 
 static int choose_chunks_tiles(int64_t n_tiles, int n_groups, int grid_full) {
@@ -556,12 +635,12 @@ void plan_k2_tiled(const pq_index_s* idx, int B, int K, K2Plan& p) {
     p.variant = 3;
     const pq_tuning& t = idx->tuning;
     const int R = idx->v3_R;
-    p.W = (t.warps == 8 || t.warps == 16) ? t.warps : 16;
+    p.W = (t.warps == 8 || t.warps == 16 || t.warps == 32) ? t.warps : 16;
     p.G = R; p.Ug = R; p.J = 1;
     p.tm = (idx->m / k2_tiled_ps(idx->m)) > 1 ? idx->m - k2_tiled_ps(idx->m) : 0;
     p.n_groups = (int)ceil_div(B, R);
     const int TR = k2_tiled_rows_per_tile(R);
-    p.cap = (int)align_up((size_t)(2 * K + TR + 32), 32);
+    p.cap = (int)align_up((size_t)(2 * K + 2 * TR + 96), 32);
     p.smem = k2_tiled_smem(idx->m, idx->b, R, p.W);
     K2TFn fn = tiled_fn(idx->m, idx->b, R, p.W);
     if (!fn) fail(PQ_ERR_UNSUPPORTED, "tiled scoring kernel: unsupported shape");
@@ -615,7 +694,14 @@ void launch_k2_tiled(const pq_index_s* idx, const K2Plan& p, int B, int K,
     a.n_groups = p.n_groups; a.chunks = p.chunks; a.chunk_tiles = p.chunk_items;
     a.ubuf = lanebuf; a.cap = p.cap; a.cand = cand;
     a.gtau = gtau_of(idx, p, St);
+    const char* dbe = getenv("PQTOPK_K2_DEBUG");
+    if (dbe && *dbe) {
+        PQ_CUDA(cudaMalloc(&a.dbg, 64 * 4));
+        PQ_CUDA(cudaMemsetAsync(a.dbg, 0, 64 * 4, st));
+    }
     const char* tf = getenv("PQTOPK_K2_TRACE");
+    const char* tsd = getenv("PQTOPK_K2_TRACE_STRIDE");
+    a.trace_stride = tsd ? std::max(1, atoi(tsd)) : 1;
     const size_t tn = (size_t)p.W * TRACE_PH * 3 + TRACE_PH;
     if (tf && *tf) {
         PQ_CUDA(cudaMalloc(&a.trace, tn * 8));
@@ -625,6 +711,14 @@ void launch_k2_tiled(const pq_index_s* idx, const K2Plan& p, int B, int K,
     fn<<<p.grid, p.W * 32, p.smem, st>>>(a);
     count_launch();
     check_launch("k2_tiled");
+    if (a.dbg) {
+        int h[16];
+        PQ_CUDA(cudaMemcpyAsync(h, a.dbg, sizeof h, cudaMemcpyDeviceToHost, st));
+        PQ_CUDA(cudaStreamSynchronize(st));
+        cudaFree(a.dbg);
+        fprintf(stderr, "k2_tiled debug: stuck=%d cta=%d warp=%d tseq=%d arrivals=%d unit=%d t=%d ntl=%d sflag=%d,%d\n",
+                h[0], h[1], h[2], h[3], h[4], h[5], h[6], h[7], h[8], h[9]);
+    }
     if (a.trace) {                       // diagnostics only: dump CTA 0's phase timeline
         std::vector<long long> h(tn);
         PQ_CUDA(cudaMemcpyAsync(h.data(), a.trace, tn * 8, cudaMemcpyDeviceToHost, st));

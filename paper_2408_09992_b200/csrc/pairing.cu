@@ -97,6 +97,40 @@ PairLayout build_pairing(const uint8_t* codes, int64_t N, int m, int b, int tm) 
     }
     L.matched_pairs = (int64_t)A.size();
     L.leftover = (int64_t)left.size();
+    // Second pass over the leftovers: pair items whose signatures differ from
+    // each other's complement in ONE split (those pairs conflict on one split
+    // only instead of about m/2).  Greedy, in ascending signature order.
+    if (m <= 20 && !left.empty()) {
+        const size_t nb = (size_t)1 << m;
+        std::vector<int64_t> head(nb, -1), nxt(left.size(), -1);
+        for (size_t t = left.size(); t-- > 0;) {
+            const uint32_t sg = sig[left[t]];
+            nxt[t] = head[sg];
+            head[sg] = (int64_t)t;
+        }
+        std::vector<uint8_t> used(left.size(), 0);
+        std::vector<int64_t> rest;
+        for (size_t t = 0; t < left.size(); ++t) {
+            if (used[t]) continue;
+            const uint32_t sg = sig[left[t]];
+            int64_t mate = -1;
+            for (int j = 0; j < m && mate < 0; ++j) {
+                const uint32_t c = (sg ^ mask) ^ (1u << j);
+                int64_t& h = head[c];
+                while (h >= 0 && used[h]) h = nxt[h];
+                if (h >= 0 && (size_t)h != t) { mate = h; }
+            }
+            used[t] = 1;
+            if (mate >= 0) {
+                used[mate] = 1;
+                A.push_back(left[t]);
+                Bv.push_back(left[mate]);
+            } else {
+                rest.push_back(left[t]);
+            }
+        }
+        left.swap(rest);
+    }
     for (size_t t = 0; t + 1 < left.size(); t += 2) { A.push_back(left[t]); Bv.push_back(left[t + 1]); }
     if (left.size() % 2) { A.push_back(left.back()); Bv.push_back(-1); }
     const int64_t np = (int64_t)A.size();

@@ -186,12 +186,17 @@ static void build_v3_layout(pq_index_s* idx, const uint8_t* codes_in, const uint
     const int ps = k2_tiled_ps(m), np = m / ps;
     std::vector<uint16_t> c3((size_t)tiles * TR * m, 0);
     std::vector<int32_t> p3((size_t)tiles * TR, -1);
+    // inside a phase block, slot pairs are interleaved: logical row rr = slot * RPS + r
+    // is stored at ((slot / 2) * RPS + r) * 2 + slot % 2 (k2_tiled.cu, CodePair)
+    const int64_t RPS = 32 / (R / 4);
     for (int64_t r = 0; r < L.rows; ++r) {
         const int64_t t = r / TR, rr = r % TR;
+        const int64_t gs = rr / RPS, ri = rr % RPS;
+        const int64_t sr = ((gs >> 1) * RPS + ri) * 2 + (gs & 1);
         p3[(size_t)r] = L.perm[(size_t)r];
         for (int ph = 0; ph < np; ++ph)
             for (int kk = 0; kk < ps; ++kk)
-                c3[(size_t)(((t * np + ph) * TR + rr) * ps + kk)] = L.codes16[(size_t)r * m + ph * ps + kk];
+                c3[(size_t)(((t * np + ph) * TR + sr) * ps + kk)] = L.codes16[(size_t)r * m + ph * ps + kk];
     }
     const size_t cbytes = c3.size() * 2 + V3_CODE_PAD;
     PQ_CUDA(cudaMalloc(&idx->d_codes3, cbytes));
@@ -373,7 +378,7 @@ pq_status pq_set_tuning(pq_index idx, const pq_tuning* t) {
     PQ_API_BEGIN
     need(idx != nullptr, "index is NULL");
     if (t) {
-        need(t->warps >= 0 && t->warps <= 16, "tuning.warps must be in [0, 16]");
+        need(t->warps >= 0 && t->warps <= 32, "tuning.warps must be in [0, 32]");
         need(t->ctas >= 0 && t->chunks >= 0 && t->variant >= 0, "tuning values must be >= 0");
         need(t->users_per_row >= 0 && t->users_per_row <= 32, "tuning.users_per_row must be in [0, 32]");
         idx->tuning = *t;

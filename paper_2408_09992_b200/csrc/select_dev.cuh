@@ -67,11 +67,20 @@ __device__ __forceinline__ uint64_t warp_kth(const uint64_t* buf, int n, uint32_
 #pragma unroll
         for (int i = lane; i < 256; i += 32) hist[i] = 0;
         __syncwarp();
-        for (int i0 = 0; i0 < n; i0 += 32) {
-            int i = i0 + lane;
-            uint64_t v = i < n ? buf[i] : 0ull;
-            bool ok = (i < n) && ((v & hmask) == prefix);
-            hist_add(hist, ok, (uint32_t)(v >> shift) & 255u);
+        constexpr int U = 4;                    // loads in flight per lane
+        for (int i0 = 0; i0 < n; i0 += 32 * U) {
+            uint64_t v[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int i = i0 + u * 32 + lane;
+                v[u] = i < n ? buf[i] : 0ull;
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int i = i0 + u * 32 + lane;
+                const bool ok = (i < n) && ((v[u] & hmask) == prefix);
+                hist_add(hist, ok, (uint32_t)(v[u] >> shift) & 255u);
+            }
         }
         __syncwarp();
         uint32_t dg, ab;

@@ -11,10 +11,10 @@ n = int(valid.sum())
 t0 = ev[:, 0, 0].min()
 ev -= t0; iss -= t0
 print(f"W={W} phases traced={n}")
-print(" ph  wait_start(min..max)   wait_len(mean,max)  end(min..max)   issue_of_this_ph  phase_len(mean)")
+print(" ph  wait_start(min..max)   wait_len(mean,max)  end(min..max)   phase_len(mean)")
 for g in range(min(n, int(sys.argv[2]) if len(sys.argv) > 2 else 40)):
     ws, we, pe = ev[:, g, 0], ev[:, g, 1], ev[:, g, 2]
-    print(f"{g:3d} {ws.min():9.0f}..{ws.max():9.0f}  {np.mean(we-ws):8.0f} {np.max(we-ws):8.0f}  {pe.min():9.0f}..{pe.max():9.0f}  {iss[g]:10.0f}  {np.mean(pe-we):8.0f}")
+    print(f"{g:3d} {ws.min():9.0f}..{ws.max():9.0f}  {np.mean(we-ws):8.0f} {np.max(we-ws):8.0f}  {pe.min():9.0f}..{pe.max():9.0f}  {np.mean(pe-we):8.0f}")
 wl = (ev[:, :n, 1] - ev[:, :n, 0]).sum() / (ev[:, :n, 2] - ev[:, :n, 0]).sum()
 print(f"fraction of warp time waiting for tables: {wl:.3f}")
 sk = (ev[:, :n, 2].max(0) - ev[:, :n, 2].min(0)).mean()
