@@ -614,19 +614,21 @@ size_t k2_tiled_smem(int m, int b, int R, int W) {
            3 * 8 + 3 * 4 + (size_t)(W + 2) * 4 + 16;
 }
 
-static int choose_chunks_tiles(int64_t n_tiles, int n_groups, int grid_full) {
+// Item chunks per user group.  Units (group x chunk) are dealt round-robin to
+// the persistent CTAs; a unit costs its tiles plus a fixed overhead (first-tile
+// shrink, end-of-unit merge and, for single-phase tables, the table load), in
+// tile units `ovh`.  Pick the chunk count with the best modelled efficiency.
+static int choose_chunks_tiles(int64_t n_tiles, int n_groups, int grid_full, double ovh) {
     const int64_t max_c = std::max<int64_t>(1, std::min<int64_t>(4096, n_tiles));
     int best = 1;
     double best_eff = -1.0;
     for (int64_t c = 1; c <= max_c; ++c) {
         const int64_t ct = ceil_div(n_tiles, c);
         const int64_t cc = ceil_div(n_tiles, ct);        // chunks actually formed
-        // work is proportional to tiles; the last chunk may be short
         const int64_t units = (int64_t)n_groups * cc;
         const int64_t per_cta = ceil_div(units, grid_full);
-        const double eff = (double)n_groups * n_tiles / ((double)per_cta * grid_full * ct);
+        const double eff = (double)n_groups * n_tiles / ((double)per_cta * grid_full * (ct + ovh));
         if (eff > best_eff + 1e-9) { best_eff = eff; best = (int)cc; }
-        if (eff >= 0.97) break;
     }
     return best;
 }
@@ -652,7 +654,8 @@ void plan_k2_tiled(const pq_index_s* idx, int B, int K, K2Plan& p) {
     const int grid_full = idx->num_sms * occ;
     const int64_t n_tiles = idx->v3_tiles;
     p.chunks = t.chunks > 0 ? (int)std::min<int64_t>(t.chunks, n_tiles)
-                            : choose_chunks_tiles(n_tiles, p.n_groups, grid_full);
+                            : choose_chunks_tiles(n_tiles, p.n_groups, grid_full,
+                                                  (idx->m / k2_tiled_ps(idx->m)) > 1 ? 0.3 : 0.6);
     const int64_t ct = ceil_div(n_tiles, p.chunks);
     p.chunk_items = ct;                                // tiles per chunk
     p.chunks = (int)ceil_div(n_tiles, ct);
