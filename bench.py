@@ -122,10 +122,8 @@ def dist_env():
 
 
 def shard(N, world, rank):
-    n = N // world
-    lo = rank * n
-    hi = N if rank == world - 1 else lo + n
-    return lo, hi
+    from paper_2408_09992_b200.dist import shard_range
+    return shard_range(N, world, rank)
 
 
 def workload_name(cfg):
@@ -184,7 +182,7 @@ def run_reference(args):
     line = {
         "impl": "reference", "metric": "user-item scores/s", "value": value, "unit": "user-item scores/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
-        "higher_is_better": True, "scaling": "strong" if world > 1 else "weak", "vs_baseline": None,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f32", "data": "synthetic (pqsynth, seeded)",
         "config": {"workload": workload_name(cfg), "users_per_step": upstep},
         "cpu_baseline": {"value": value, "unit": "user-item scores/s", "cores": oracle.max_threads(),
@@ -239,21 +237,22 @@ def run_ours(args):
     sc = torch.empty((B, K), dtype=torch.float32, device=dev)
     ws = torch.empty(idx.topk_workspace_bytes(B, K), dtype=torch.uint8, device=dev)
     if world > 1:
-        g_ids = torch.empty((world, B, K), dtype=torch.int32, device=dev)
-        g_sc = torch.empty((world, B, K), dtype=torch.float32, device=dev)
         out_ids = torch.empty((B, K), dtype=torch.int32, device=dev)
         out_sc = torch.empty((B, K), dtype=torch.float32, device=dev)
         mws_n = int(pq.load_library().pq_merge_workspace_bytes(world, B, K))
         mws = torch.empty(max(mws_n, 1), dtype=torch.uint8, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
+    from paper_2408_09992_b200.dist import gather_merge
+
+    def merge_into_out(gi, gs):
+        return pq.pq_merge_topk(gi, gs, ws=mws, out_ids=out_ids, out_scores=out_sc)
+
     def step():
         pq.pq_subscores(F_d, P_d, S)
         pq.pq_score_topk(idx, S, K, ws=ws, ids=ids, scores=sc)
-        if world > 1:
-            dist.all_gather_into_tensor(g_ids, ids)
-            dist.all_gather_into_tensor(g_sc, sc)
-            pq.pq_merge_topk(g_ids, g_sc, ws=mws, out_ids=out_ids, out_scores=out_sc)
+        if world > 1:                                # NCCL all-gather of B x K + merge (dist.py)
+            gather_merge(ids, sc, merge=merge_into_out)
 
     def barrier():
         if world > 1:
@@ -304,9 +303,7 @@ def run_ours(args):
             pq.pq_search(idx, F_h, P_h, K, ws=sws, ids=ids_h, scores=sc_h)
         else:
             pq.pq_search(idx, F_h, P_h, K, ws=sws, ids=ids, scores=sc)
-            dist.all_gather_into_tensor(g_ids, ids)
-            dist.all_gather_into_tensor(g_sc, sc)
-            pq.pq_merge_topk(g_ids, g_sc, ws=mws, out_ids=out_ids, out_scores=out_sc)
+            gather_merge(ids, sc, merge=merge_into_out)
             ids_h.copy_(out_ids, non_blocking=True)
             sc_h.copy_(out_sc, non_blocking=True)
     for _ in range(max(1, args.warmup)):

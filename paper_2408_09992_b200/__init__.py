@@ -26,6 +26,8 @@ from .binding import (  # noqa: F401
     pq_subscores,
 )
 
+from . import dist  # noqa: F401,E402  (item sharding across GPUs)
+
 __all__ = [
     "PQError", "PQIndex", "Tuning", "abi_version", "launch_count", "lib_path", "load_library",
     "pq_create", "pq_subscores", "pq_score_topk", "pq_search", "pq_merge_topk",
