@@ -347,11 +347,15 @@ def run_ours(args):
     if os.path.exists(tp):
         traffic = json.load(open(tp)).get("dram_bytes_per_launch")
     roofline = {
-        "bound": "smem", "kernel": "k2_score_select (fused gather-sum-select)",
+        "bound": "smem",
+        "kernel": {1: "k2_score_select (v1 row groups)", 2: "k2_paired (v2)",
+                   3: "k2_tiled (v3: fused gather-sum-select, 4 users/lane)"}.get(plan["variant"], "k2"),
         "achieved": achieved / 1e9, "peak": peak_lookups / 1e9, "unit": "G lookups/s",
         "frac": achieved / peak_lookups, "traffic": traffic,
         "achieved_GBps_smem": achieved * 4 / 1e9, "peak_GBps_smem": peak_lookups * 4 / 1e9,
-        "peak_source": f"{nsm} SMs x 32 banks x 4 B x {f_max:.0f} MHz (sm_max_mhz, {pk['source']})",
+        "peak_source": f"{nsm} SMs x 32 banks x 4 B x {f_max:.0f} MHz (sm_max_mhz, {pk['source']}); "
+                       "128 B/clk/SM attained by the paired LDS.128 pattern in the smem microbenchmark "
+                       "(profiles/r01/ubench/smem_rate_b200.txt)",
         "per_launch": {"lookups": lookups, "algorithmic_hbm_bytes": n_local * m + B * m * b * 4 + B * K * 8,
                        "k2_ms": k2_avg_s * 1e3},
         "k2_share_of_step": (k2_ms_max / args.steps) / ms_per_step,
