@@ -75,7 +75,8 @@ struct K2TArgs {
     int trace_stride;          // trace every trace_stride-th tile (PQTOPK_K2_TRACE_STRIDE)
     int* dbg;                  // diagnostics (PQTOPK_K2_DEBUG): bounded spins record state here
 };
-constexpr int TRACE_PH = 256;  // traced table uses (CTA 0): [W][TRACE_PH][3] + issue [TRACE_PH]
+constexpr int TRACE_PH = 256;  // traced table uses (CTA 0): [W][TRACE_PH][3]; then CTA 0 units [TRACE_PH/2][2];
+constexpr int TRACE_CTAS = 1024;  // then per-CTA [TRACE_CTAS][3] = (start ns, end ns, tiles)
 
 // ---------------------------------------------------------------- PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -342,7 +343,15 @@ __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
     const int wm = a.cap - 2 * TR - 32;
     int64_t tseq = 0;                                  // tiles done by this CTA
 
+    constexpr int64_t PSTR = 2 * RPS * CB;             // code bytes per slot pair
+    constexpr int DP = D / 2;                          // slot pairs per group
+    __shared__ unsigned long long t_start_ns;
+    if (a.trace && threadIdx.x == 0) {
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start_ns));
+    }
     for (int64_t unit = blockIdx.x; unit < units; unit += gridDim.x) {
+        if (a.trace && blockIdx.x == 0 && threadIdx.x == 0 && useq < TRACE_PH / 2)
+            a.trace[(int64_t)W * TRACE_PH * 3 + 2 * useq] = clock64();
         const int chunk = (int)(unit / a.n_groups);
         const int grp = (int)(unit - (int64_t)chunk * a.n_groups);
         const int64_t tile0 = (int64_t)chunk * a.chunk_tiles;
@@ -373,8 +382,6 @@ __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
                 // codes of this warp's slot pairs: [pair][row][2 slots][PS]
                 const char* cp = reinterpret_cast<const char*>(a.codes) + ((tile * NP + ph) * TR +
                                  ((int64_t)warp * SL * RPS + (lane / LPR) * 2)) * CB;
-                constexpr int64_t PSTR = 2 * RPS * CB;  // bytes per slot pair
-                constexpr int DP = D / 2;               // slot pairs per group
                 CodePair<PS> cw[DP];
 #pragma unroll
                 for (int d = 0; d < DP; ++d) cw[d].load(cp + d * PSTR);
@@ -543,7 +550,15 @@ __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
         }
         __syncthreads();
         if (threadIdx.x < R) { tau_sh[threadIdx.x] = 0ull; cnt_u[threadIdx.x] = 0; nconv_u[threadIdx.x] = 0; }
+        if (a.trace && blockIdx.x == 0 && threadIdx.x == 0 && useq < TRACE_PH / 2)
+            a.trace[(int64_t)W * TRACE_PH * 3 + 2 * useq + 1] = clock64();
         ++useq;
+    }
+    if (a.trace && threadIdx.x == 0 && blockIdx.x < TRACE_CTAS) {
+        unsigned long long t_end_ns;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end_ns));
+        long long* c = a.trace + (int64_t)W * TRACE_PH * 3 + TRACE_PH + 3 * blockIdx.x;
+        c[0] = (long long)t_start_ns; c[1] = (long long)t_end_ns; c[2] = tseq;
     }
 
     if constexpr (NP > 1) {
@@ -705,7 +720,7 @@ void launch_k2_tiled(const pq_index_s* idx, const K2Plan& p, int B, int K,
     const char* tf = getenv("PQTOPK_K2_TRACE");
     const char* tsd = getenv("PQTOPK_K2_TRACE_STRIDE");
     a.trace_stride = tsd ? std::max(1, atoi(tsd)) : 1;
-    const size_t tn = (size_t)p.W * TRACE_PH * 3 + TRACE_PH;
+    const size_t tn = (size_t)p.W * TRACE_PH * 3 + TRACE_PH + 3 * TRACE_CTAS;
     if (tf && *tf) {
         PQ_CUDA(cudaMalloc(&a.trace, tn * 8));
         PQ_CUDA(cudaMemsetAsync(a.trace, 0, tn * 8, st));
