@@ -65,7 +65,8 @@ typedef enum {
  * results; this exists for tests (F12: two geometries, same bits) and tuning. */
 typedef struct {
     int32_t variant;     /* 0 auto; 1 = generic row-group kernel; 2 = paired half-warps;
-                            3 = tiled phases (4 users per lane, TMA tables, TMEM partials) */
+                            3 = tiled phases (4 users per lane, TMA tables, TMEM partials);
+                            4 = small-batch latency kernel (B <= 4, lane = item) */
     int32_t ctas;        /* persistent CTAs of the scoring kernel (0 = #SMs x occupancy) */
     int32_t warps;       /* warps per CTA of the scoring kernel (0 = auto) */
     int32_t chunks;      /* item chunks per user group (0 = auto) */
@@ -123,7 +124,7 @@ pq_status pq_index_variants(pq_index idx, int32_t* mask);
 
 /*
  * The launch plan pq_score_topk would use for (B, K) (diagnostics):
- * out[0] variant (1 row groups, 2 paired half-warps, 3 tiled phases), out[1] users per table row
+ * out[0] variant (1 row groups, 2 paired half-warps, 3 tiled phases, 4 small batch), out[1] users per table row
  * (G), out[2] users per group, out[3] warps per CTA, out[4] CTAs, out[5] item
  * chunks, out[6] TMEM splits, out[7] dynamic shared memory bytes.
  */

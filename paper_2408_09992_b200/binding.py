@@ -187,10 +187,11 @@ class PQIndex:
                 "leftover_items": lo.value}
 
     def variants(self):
-        """Set of K2 scoring variants this index supports (1 generic, 2 paired, 3 tiled)."""
+        """Set of K2 scoring variants this index supports (1 generic, 2 paired, 3 tiled,
+        4 small-batch latency)."""
         m = ctypes.c_int32()
         _check(load_library().pq_index_variants(self._h, ctypes.byref(m)))
-        return {v for v in (1, 2, 3) if m.value >> v & 1}
+        return {v for v in (1, 2, 3, 4) if m.value >> v & 1}
 
     def plan(self, B: int, K: int):
         """The K2 launch plan for (B, K) as a dict (diagnostics)."""

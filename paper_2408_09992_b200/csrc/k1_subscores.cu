@@ -12,8 +12,9 @@
 // so it stays SIMT fp64 (TF32/BF16 tensor cores would break the tolerance; see
 // DESIGN.md "K1").
 //
-// Grid: (m, ceil(B/UB)); a block stages psi_k (b x TT tile, padded rows) and
-// phi_k for UB users in shared memory and produces the UB x b outputs.
+// Grid: (m, ceil(B/UB), ceil(b/gchunk)); a block stages psi_k (gchunk x TT tile,
+// padded rows) and phi_k for UB users in shared memory and produces the UB x
+// gchunk outputs (gchunk = b, or 32 for small batches to fill the GPU).
 #include "pq_internal.cuh"
 
 namespace pq {
@@ -24,14 +25,16 @@ constexpr int K1_THREADS = 256;
 
 __global__ void __launch_bounds__(K1_THREADS)
 k1_subscores(const float* __restrict__ phi, const float* __restrict__ psi, int B, int d,
-             int m, int b, float* __restrict__ S) {
+             int m, int b, float* __restrict__ S, int gchunk) {
     __shared__ float ps[256 * (K1_TT + 1)];
     __shared__ float fs[K1_UB * K1_TT];
     const int k = blockIdx.x;
     const int u0 = blockIdx.y * K1_UB;
     const int nu = min(K1_UB, B - u0);
     const int dm = d / m;
-    const int nout = nu * b;
+    const int g0 = blockIdx.z * gchunk;             // sub-ids [g0, g0 + nb) of split k
+    const int nb = min(gchunk, b - g0);
+    const int nout = nu * nb;
     constexpr int PER = (K1_UB * 256 + K1_THREADS - 1) / K1_THREADS;   // <= 16
     double acc[PER];
 #pragma unroll
@@ -40,9 +43,9 @@ k1_subscores(const float* __restrict__ phi, const float* __restrict__ psi, int B
     for (int t0 = 0; t0 < dm; t0 += K1_TT) {
         const int tt = min(K1_TT, dm - t0);
         __syncthreads();
-        for (int x = threadIdx.x; x < b * tt; x += K1_THREADS) {
+        for (int x = threadIdx.x; x < nb * tt; x += K1_THREADS) {
             int g = x / tt, t = x - g * tt;
-            ps[g * (K1_TT + 1) + t] = psi[((int64_t)k * b + g) * dm + t0 + t];
+            ps[g * (K1_TT + 1) + t] = psi[((int64_t)k * b + g0 + g) * dm + t0 + t];
         }
         for (int x = threadIdx.x; x < nu * tt; x += K1_THREADS) {
             int u = x / tt, t = x - u * tt;
@@ -53,7 +56,7 @@ k1_subscores(const float* __restrict__ phi, const float* __restrict__ psi, int B
         for (int j = 0; j < PER; ++j) {
             int o = threadIdx.x + j * K1_THREADS;
             if (o < nout) {
-                int u = o / b, g = o - u * b;
+                int u = o / nb, g = o - u * nb;
                 const float* pr = ps + g * (K1_TT + 1);
                 const float* fr = fs + u * K1_TT;
                 double a = acc[j];
@@ -67,8 +70,8 @@ k1_subscores(const float* __restrict__ phi, const float* __restrict__ psi, int B
     for (int j = 0; j < PER; ++j) {
         int o = threadIdx.x + j * K1_THREADS;
         if (o < nout) {
-            int u = o / b, g = o - u * b;
-            S[((int64_t)(u0 + u) * m + k) * b + g] = (float)acc[j];   // one rounding (RN)
+            int u = o / nb, g = o - u * nb;
+            S[((int64_t)(u0 + u) * m + k) * b + g0 + g] = (float)acc[j];   // one rounding (RN)
         }
     }
 }
@@ -76,8 +79,10 @@ k1_subscores(const float* __restrict__ phi, const float* __restrict__ psi, int B
 void launch_subscores(const float* phi, const float* psi, int B, int d, int m, int b,
                       float* S, cudaStream_t st) {
     if (B <= 0) return;
-    dim3 grid(m, (unsigned)ceil_div(B, K1_UB));
-    k1_subscores<<<grid, K1_THREADS, 0, st>>>(phi, psi, B, d, m, b, S);
+    // small batches: also split the sub-ids over blocks (more blocks in flight)
+    const int gchunk = B <= 64 ? std::min(b, 32) : b;
+    dim3 grid(m, (unsigned)ceil_div(B, K1_UB), (unsigned)ceil_div(b, gchunk));
+    k1_subscores<<<grid, K1_THREADS, 0, st>>>(phi, psi, B, d, m, b, S, gchunk);
     count_launch();
     check_launch("k1_subscores");
 }

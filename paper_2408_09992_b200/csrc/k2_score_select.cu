@@ -259,6 +259,11 @@ K2Plan plan_k2(const pq_index_s* idx, int B, int K) {
         plan_k2_tiled(idx, B, K, p);
         return p;
     }
+    if ((tt.variant == 4 || (tt.variant == 0 && tt.users_per_row == 0)) && k2_latency_supported(idx, B, K)) {
+        K2Plan p;
+        plan_k2_latency(idx, B, K, p);
+        return p;
+    }
     if (idx->v2_ok && tt.variant != 1 && tt.users_per_row == 0 && (B >= 16 || tt.variant == 2))
         return plan_k2_paired(idx, B, K);
     K2Plan p;

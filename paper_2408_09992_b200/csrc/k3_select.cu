@@ -59,6 +59,24 @@ k3_select(Src src, int64_t L, int K, int Kp, uint64_t* __restrict__ out_keys,
     const int tid = threadIdx.x;
 
     for (int i = tid; i < n; i += blockDim.x) keys[i] = src.get(u, e0 + i);
+    if (n <= 1024) {
+        // short lists (small batches, the B x P x K merges): sort them whole
+        const int P = pow2_ceil(n > 0 ? n : 1);
+        for (int i = n + tid; i < P; i += blockDim.x) keys[i] = 0ull;
+        __syncthreads();
+        block_bitonic_desc(keys, P);
+        if (out_ids) {
+            for (int j = tid; j < K; j += blockDim.x) {
+                const uint64_t v = j < P ? keys[j] : 0ull;
+                out_ids[(int64_t)u * K + j] = v ? key_id(v) : -1;
+                out_sc[(int64_t)u * K + j] = v ? key_score(v) : -INFINITY;
+            }
+        } else {
+            uint64_t* o = out_keys + ((int64_t)u * out_lists + list_off + s) * K;
+            for (int j = tid; j < K; j += blockDim.x) o[j] = j < P ? keys[j] : 0ull;
+        }
+        return;
+    }
     for (int i = tid; i < Kp; i += blockDim.x) sel[i] = 0ull;
     if (tid == 0) sh[2] = 0;
     __syncthreads();

@@ -84,6 +84,7 @@ static void run_score_topk(pq_index_s* idx, const float* S, int B, int K, void* 
         PQ_CUDA(cudaEventRecord(ev.a, st));
     }
     if (w.plan.variant == 3) launch_k2_tiled(idx, w.plan, B, K, lanebuf, mscr, St, cand, st);
+    else if (w.plan.variant == 4) launch_k2_latency(idx, w.plan, S, B, K, cand, st);
     else launch_k2(idx, w.plan, S, B, K, lanebuf, cand, st);
     if (idx->timing) PQ_CUDA(cudaEventRecord(ev.b, st));
     k3_keys_to_topk(cand, (int64_t)w.plan.chunks * K, B, K, k3s, ids, scores, st);
@@ -359,7 +360,7 @@ pq_status pq_index_layout(pq_index idx, int32_t* paired, int32_t* tmem_splits,
 pq_status pq_index_variants(pq_index idx, int32_t* mask) {
     PQ_API_BEGIN
     need(idx != nullptr && mask != nullptr, "NULL argument");
-    *mask = 2 | (idx->v2_ok ? 4 : 0) | (idx->v3_ok ? 8 : 0);
+    *mask = 2 | (idx->v2_ok ? 4 : 0) | (idx->v3_ok ? 8 : 0) | (k2_latency_supported(idx, 1, 1) ? 16 : 0);
     PQ_API_END
 }
 

@@ -132,6 +132,11 @@ struct K2Plan {
     int tm = 0;
     size_t st_bytes = 0;          // v3: tiled S tables [n_groups][m][b][16] fp32
 };
+// v4 helpers (k2_latency.cu): small batches (B <= 4), lane = item
+bool k2_latency_supported(const pq_index_s* idx, int B, int K);
+void plan_k2_latency(const pq_index_s* idx, int B, int K, K2Plan& p);
+void launch_k2_latency(const pq_index_s* idx, const K2Plan& p, const float* S, int B, int K,
+                       uint64_t* cand, cudaStream_t st);
 // v3 helpers (k2_tiled.cu)
 bool k2_tiled_supported(int m, int b);
 int k2_tiled_users(int m, int b);

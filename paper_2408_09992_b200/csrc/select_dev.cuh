@@ -108,6 +108,60 @@ __device__ __forceinline__ uint64_t warp_kth(const uint64_t* buf, int n, uint32_
     return prefix;
 }
 
+// Block-level: the K-th largest of keys buf[0..n) in SHARED memory (n >= K >= 1),
+// all threads of the block call it.  MSD radix select (8 bits per pass,
+// warp-aggregated histogram increments, early exit as in warp_kth).  hist: 256
+// words of shared memory; sc: 4 shared words of scratch.  Returns the key in
+// every thread.
+__device__ __forceinline__ uint64_t block_kth(const uint64_t* buf, int n, uint32_t K, uint32_t* hist,
+                                              unsigned long long* sc) {
+    uint64_t prefix = 0;
+    uint32_t krem = K;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int shift = 56; shift >= 0; shift -= 8) {
+        const uint64_t hmask = (shift == 56) ? 0ull : (~0ull << (shift + 8));
+        for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
+        __syncthreads();
+        for (int i0 = 0; i0 < n; i0 += blockDim.x) {
+            const int i = i0 + threadIdx.x;
+            const uint64_t v = i < n ? buf[i] : 0ull;
+            const bool ok = (i < n) && ((v & hmask) == prefix);
+            hist_add(hist, ok, (uint32_t)(v >> shift) & 255u);
+        }
+        __syncthreads();
+        if (warp == 0) {
+            uint32_t dg, ab;
+            warp_find_digit(hist, krem, dg, ab);
+            if (lane == 0) { sc[0] = dg; sc[1] = ab; sc[2] = hist[dg]; sc[3] = ~0ull; }
+        }
+        __syncthreads();
+        const uint32_t dg = (uint32_t)sc[0], ab = (uint32_t)sc[1], inbin = (uint32_t)sc[2];
+        prefix |= (uint64_t)dg << shift;
+        krem -= ab;
+        if (shift > 0 && inbin == krem) {        // the K-th is the smallest key of the bin
+            const uint64_t pmask = ~0ull << shift;
+            uint64_t mn = ~0ull;
+            for (int i = threadIdx.x; i < n; i += blockDim.x) {
+                const uint64_t v = buf[i];
+                if ((v & pmask) == prefix && v < mn) mn = v;
+            }
+#pragma unroll
+            for (int o = 16; o; o >>= 1) {
+                const uint64_t t = __shfl_xor_sync(FULL, mn, o);
+                mn = t < mn ? t : mn;
+            }
+            __syncthreads();                      // everyone has read sc[0..2]
+            if (lane == 0) atomicMin(&sc[3], (unsigned long long)mn);
+            __syncthreads();
+            const uint64_t r = sc[3];
+            __syncthreads();
+            return r;
+        }
+        __syncthreads();                          // sc is rewritten by the next pass
+    }
+    return prefix;
+}
+
 // Block-level bitonic sort (descending) of s[0..n), n a power of two.
 __device__ __forceinline__ void block_bitonic_desc(uint64_t* s, int n) {
     for (int size = 2; size <= n; size <<= 1) {

@@ -58,6 +58,8 @@ CONFIGS = {
                  note="latency regime (PAPER.md:259 elbow)"),
     "c2": Config("c2", 2, 1_280_000, 8, 256, 512, 128, 10, psi_sigma=0.02,
                  note="Gowalla-shaped (PAPER.md:173); B=1 is row 0 of B=128"),
+    "c2a": Config("c2a", 2, 1_280_000, 8, 256, 512, 1, 10, psi_sigma=0.02,
+                  note="Gowalla-shaped single user: row 0 of c2 (same cfg_id -> same codes/Psi)"),
     "c3": Config("c3", 3, 10_000_000, 8, 256, 512, 256, 100, codes="zipf",
                  note="Zipf(1.1) codes per split"),
     "c4": Config("c4", 4, 50_000_000, 16, 256, 512, 1024, 100, gpus=(1, 2, 4, 8),

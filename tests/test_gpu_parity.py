@@ -278,7 +278,7 @@ def test_paired_layout_matches_generic(pq, torch, orc, m, B, dist):
     idx = pq.pq_create(G, b=256, id_base=3)
     lay = idx.layout()
     assert lay["paired"] == 1 and lay["tmem_splits"] == (2 if m == 16 else 0)
-    assert idx.variants() == {1, 2, 3}
+    assert idx.variants() == {1, 2, 3, 4}
     if dist == "uniform":
         assert lay["leftover_items"] < 0.2 * G.shape[0]
     S_t = pq.pq_subscores(cuda(torch, F), cuda(torch, P))
@@ -336,5 +336,32 @@ def test_tiled_parity(pq, torch, orc, case):
     for tun in (dict(variant=3), dict(variant=3, warps=8, ctas=3, chunks=5)):
         idx.set_tuning(**tun)
         assert idx.plan(B, K)["variant"] == 3
+        i, s = pq.pq_score_topk(idx, S_t, K)
+        assert_same(i.cpu().numpy(), s.cpu().numpy(), *ref, str(tun))
+
+
+LATENCY_CASES = [
+    # seed, N, m, b, B, K, dist — the serving case (B <= 4)
+    (500, 10_000, 8, 256, 1, 10, "uniform"),        # C1 shape
+    (501, 1_280_000, 8, 256, 1, 10, "uniform"),     # C2a shape
+    (502, 70_001, 16, 256, 3, 100, "uniform"),
+    (503, 50_000, 4, 16, 2, 512, "uniform"),        # heavy exact ties
+    (504, 7, 8, 256, 4, 10, "uniform"),             # K > N
+    (505, 40_000, 8, 256, 1, 1, "few"),
+]
+
+
+@pytest.mark.parametrize("case", LATENCY_CASES, ids=[str(c[0]) for c in LATENCY_CASES])
+def test_latency_parity(pq, torch, orc, case):
+    """K2 v4 (small-batch, lane = item, CTA-wide exact selection) is bit-exact
+    against the oracle given S, in two launch geometries."""
+    seed, N, m, b, B, K, dist = case
+    G, P, F = pqsynth.random_instance(seed, N, m, b, 4 * m, B, code_dist=dist)
+    idx = pq.pq_create(G, b=b, id_base=seed)
+    S_t = pq.pq_subscores(cuda(torch, F), cuda(torch, P))
+    ref = orc.pq_topk(G, S_t.cpu().numpy(), K, id_base=seed)
+    assert idx.plan(B, K)["variant"] == 4
+    for tun in (dict(), dict(variant=4, chunks=3, ctas=2)):
+        idx.set_tuning(**tun)
         i, s = pq.pq_score_topk(idx, S_t, K)
         assert_same(i.cpu().numpy(), s.cpu().numpy(), *ref, str(tun))
