@@ -164,6 +164,38 @@ pq_status pq_score_topk(pq_index idx, const float* S, int32_t B, int32_t K,
                         void* ws, size_t ws_bytes, int32_t* ids, float* scores,
                         void* stream);
 
+/*
+ * pq_score_topk_subset — PQTopK over an item subset V (Alg. 1's input V,
+ * P:119; SPEC "subset consistency"): the result is exactly the
+ * full-catalogue ranking restricted to V, cut to K.
+ *   V   : int32 [nV], device; LOCAL item ids (0 <= V[r] < N), strictly
+ *         increasing; shared by the B users.  nV == 0: every row is padding.
+ *   other arguments as pq_score_topk (ids returned are global ids).
+ * Validates V on the device and synchronises `stream` (PQ_ERR_INVALID_ARG
+ * names the first bad position).  Workspace: pq_subset_workspace_bytes.
+ */
+size_t pq_subset_workspace_bytes(pq_index idx, int64_t nV, int32_t B, int32_t K);
+pq_status pq_score_topk_subset(pq_index idx, const float* S, int32_t B, int32_t K,
+                               const int32_t* V, int64_t nV, void* ws, size_t ws_bytes,
+                               int32_t* ids, float* scores, void* stream);
+
+/*
+ * pq_score_topk_exclude — PQTopK over I minus a per-user exclusion list (e.g.
+ * the items a user has already interacted with; V_u = I \ excl_u in Alg. 1).
+ *   excl     : int32, device; user u's excluded GLOBAL ids are
+ *              excl[excl_off[u] .. excl_off[u+1]), sorted ascending.
+ *   excl_off : int64 [B + 1], device.
+ *   max_excl : >= every user's list length (the caller knows it; it sizes the
+ *              internal top-(K + max_excl) pass).  K + max_excl <= PQTOPK_MAX_K.
+ * Exact: the top-(K + max_excl) of I contains the top-K of I minus any
+ * max_excl items.  Workspace: pq_exclude_workspace_bytes.
+ */
+size_t pq_exclude_workspace_bytes(pq_index idx, int32_t B, int32_t K, int32_t max_excl);
+pq_status pq_score_topk_exclude(pq_index idx, const float* S, int32_t B, int32_t K,
+                                const int32_t* excl, const int64_t* excl_off, int32_t max_excl,
+                                void* ws, size_t ws_bytes, int32_t* ids, float* scores,
+                                void* stream);
+
 /* Workspace bytes for pq_search (pq_subscores + pq_score_topk in one call). */
 size_t pq_search_workspace_bytes(pq_index idx, int32_t B, int32_t d, int32_t K);
 

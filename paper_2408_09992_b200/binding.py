@@ -28,7 +28,9 @@ EXPORTS = ["pq_abi_version", "pq_last_error", "pq_launch_count", "pq_create", "p
            "pq_index_info", "pq_index_layout", "pq_index_variants", "pq_plan_info", "pq_set_tuning", "pq_subscores", "pq_topk_workspace_bytes",
            "pq_score_topk", "pq_search_workspace_bytes", "pq_search", "pq_merge_workspace_bytes",
            "pq_merge_topk", "pq_reconstruct", "pq_dense_workspace_bytes", "pq_dense_topk",
-           "pq_recjpq_workspace_bytes", "pq_recjpq_topk", "pq_timing_enable", "pq_timing_read"]
+           "pq_recjpq_workspace_bytes", "pq_recjpq_topk", "pq_timing_enable", "pq_timing_read",
+           "pq_subset_workspace_bytes", "pq_score_topk_subset", "pq_exclude_workspace_bytes",
+           "pq_score_topk_exclude"]
 
 
 class PQError(RuntimeError):
@@ -75,6 +77,10 @@ def load_library():
         "pq_subscores": (st, [P, P, I32, I32, I32, I32, P, P]),
         "pq_topk_workspace_bytes": (SZ, [P, I32, I32]),
         "pq_score_topk": (st, [P, P, I32, I32, P, SZ, P, P, P]),
+        "pq_subset_workspace_bytes": (SZ, [P, I64, I32, I32]),
+        "pq_score_topk_subset": (st, [P, P, I32, I32, P, I64, P, SZ, P, P, P]),
+        "pq_exclude_workspace_bytes": (SZ, [P, I32, I32, I32]),
+        "pq_score_topk_exclude": (st, [P, P, I32, I32, P, P, I32, P, SZ, P, P, P]),
         "pq_search_workspace_bytes": (SZ, [P, I32, I32, I32]),
         "pq_search": (st, [P, P, P, I32, I32, I32, P, SZ, P, P, P]),
         "pq_merge_workspace_bytes": (SZ, [I32, I32, I32]),
@@ -269,6 +275,66 @@ def pq_score_topk(index: PQIndex, S, K: int, ws=None, ids=None, scores=None, str
                            ctypes.c_void_p(_ptr(ws) if ws is not None else 0), wsb,
                            ctypes.c_void_p(_ptr(ids)), ctypes.c_void_p(_ptr(scores)),
                            ctypes.c_void_p(_stream(stream))))
+    return ids, scores
+
+
+def pq_score_topk_subset(index: PQIndex, S, K: int, V, ws=None, ids=None, scores=None, stream=None):
+    """PQTopK over the item subset V (Alg. 1 input V): V = sorted unique
+    LOCAL item ids (int32 CUDA tensor), shared by the batch."""
+    torch = _torch()
+    _need_cuda(S, "S")
+    B = int(S.shape[0])
+    dev = S.device
+    V = V.to(device=dev, dtype=torch.int32).contiguous()
+    nV = int(V.numel())
+    if ids is None:
+        ids = torch.empty((B, K), dtype=torch.int32, device=dev)
+    if scores is None:
+        scores = torch.empty((B, K), dtype=torch.float32, device=dev)
+    L = load_library()
+    nb = int(L.pq_subset_workspace_bytes(index.handle, nV, B, K)) if B > 0 and 0 < K <= MAX_K and nV > 0 else 0
+    ws, wsb = _ws(nb, ws, dev)
+    _check(L.pq_score_topk_subset(index.handle, ctypes.c_void_p(_ptr(S)), B, K,
+                                  ctypes.c_void_p(_ptr(V) if nV else 0), nV,
+                                  ctypes.c_void_p(_ptr(ws) if ws is not None else 0), wsb,
+                                  ctypes.c_void_p(_ptr(ids)), ctypes.c_void_p(_ptr(scores)),
+                                  ctypes.c_void_p(_stream(stream))))
+    return ids, scores
+
+
+def pq_score_topk_exclude(index: PQIndex, S, K: int, excluded, ws=None, ids=None, scores=None,
+                          stream=None):
+    """PQTopK over I minus a per-user exclusion list.  `excluded`: a sequence of
+    B arrays of GLOBAL item ids (any order; duplicates allowed), or a tuple
+    (excl int32 CUDA tensor sorted per user, excl_off int64 CUDA tensor [B+1])."""
+    torch = _torch()
+    _need_cuda(S, "S")
+    B = int(S.shape[0])
+    dev = S.device
+    if isinstance(excluded, tuple):
+        excl, off = excluded
+        off_h = off.cpu().numpy()
+    else:
+        lists = [np.unique(np.asarray(e, dtype=np.int64)).astype(np.int32) for e in excluded]
+        if len(lists) != B:
+            raise ValueError("one exclusion list per user")
+        off_h = np.zeros(B + 1, np.int64)
+        off_h[1:] = np.cumsum([len(x) for x in lists])
+        excl = torch.from_numpy(np.concatenate(lists) if off_h[-1] else np.zeros(1, np.int32)).to(dev)
+        off = torch.from_numpy(off_h).to(dev)
+    max_excl = int(np.max(np.diff(off_h))) if B > 0 else 0
+    if ids is None:
+        ids = torch.empty((B, K), dtype=torch.int32, device=dev)
+    if scores is None:
+        scores = torch.empty((B, K), dtype=torch.float32, device=dev)
+    L = load_library()
+    nb = int(L.pq_exclude_workspace_bytes(index.handle, B, K, max_excl)) if B > 0 and K > 0 else 0
+    ws, wsb = _ws(nb, ws, dev)
+    _check(L.pq_score_topk_exclude(index.handle, ctypes.c_void_p(_ptr(S)), B, K,
+                                   ctypes.c_void_p(_ptr(excl)), ctypes.c_void_p(_ptr(off)), max_excl,
+                                   ctypes.c_void_p(_ptr(ws) if ws is not None else 0), wsb,
+                                   ctypes.c_void_p(_ptr(ids)), ctypes.c_void_p(_ptr(scores)),
+                                   ctypes.c_void_p(_stream(stream))))
     return ids, scores
 
 

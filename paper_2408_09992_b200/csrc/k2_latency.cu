@@ -23,6 +23,7 @@ namespace pq {
 
 struct K2LArgs {
     const uint8_t* codes;      // [N][mp] item-order uint8 rows (K0 layout)
+    const int32_t* perm;       // row -> local item id (subset scoring), or null (identity)
     const float* S;            // [B][m][b]
     int64_t N;
     int mp, b, B, K;
@@ -113,7 +114,8 @@ __global__ void __launch_bounds__(K2L_THREADS) k2_latency(const K2LArgs a) {
                     const uint32_t g = (cw[j][k >> 2] >> (8 * (k & 3))) & 0xFFu;
                     acc = acc + Tl[((size_t)k * a.b + g) * G];
                 }
-                keys[j] = (item < i1 && acc >= tf) ? make_key(acc + 0.0f, a.id_base + (uint32_t)item) : 0ull;
+                const uint32_t lid = (item < i1 && a.perm) ? (uint32_t)a.perm[item] : (uint32_t)item;
+                keys[j] = (item < i1 && acc >= tf) ? make_key(acc + 0.0f, a.id_base + lid) : 0ull;
             }
             // append this round's candidates (warp-aggregated slots)
 #pragma unroll
@@ -239,6 +241,7 @@ void launch_k2_latency(const pq_index_s* idx, const K2Plan& p, const float* S, i
                        uint64_t* cand, cudaStream_t st) {
     K2LArgs a{};
     a.codes = idx->d_codes;
+    a.perm = idx->lay.paired ? idx->d_perm : nullptr;
     a.S = S;
     a.N = idx->N;
     a.mp = idx->lay.mp; a.b = idx->b; a.B = B; a.K = K;

@@ -94,6 +94,25 @@ static void run_score_topk(pq_index_s* idx, const float* S, int B, int K, void* 
     }
 }
 
+// A temporary item-order catalogue over the subset V (k5_subset.cu): row r is
+// item V[r]; only the generic (v1) and small-batch (v4) kernels read it.
+static pq_index_s subset_index(const pq_index_s* idx, int64_t nV, uint8_t* codesV, const int32_t* V) {
+    pq_index_s t{};
+    t.N = nV; t.m = idx->m; t.b = idx->b; t.id_base = idx->id_base;
+    t.device = idx->device; t.num_sms = idx->num_sms; t.smem_optin = idx->smem_optin;
+    t.lay.mp = idx->lay.mp;
+    t.lay.paired = 1;                                  // rows -> items through d_perm (= V)
+    t.d_codes = codesV;
+    t.d_perm = const_cast<int32_t*>(V);
+    t.n_rows = nV;
+    t.tuning = idx->tuning;
+    if (t.tuning.variant == 2 || t.tuning.variant == 3) t.tuning.variant = 0;
+    return t;
+}
+static size_t subset_codes_bytes(const pq_index_s* idx, int64_t nV) {
+    return align_up((size_t)nV * idx->lay.mp + 64, 256) + 256;
+}
+
 static void check_topk_args(int B, int K) {
     need(B >= 0, "B must be >= 0");
     need(K >= 0, "K must be >= 0");
@@ -578,6 +597,89 @@ pq_status pq_recjpq_topk(pq_index idx, const float* S, int32_t B, int32_t K, voi
                         lists, 0, st);
     }
     k3_keys_to_topk(keys, lists * K, B, K, k3s, ids, scores, st);
+    PQ_API_END
+}
+
+size_t pq_subset_workspace_bytes(pq_index idx, int64_t nV, int32_t B, int32_t K) {
+    try {
+        if (!idx || nV <= 0 || B <= 0 || K <= 0 || K > PQTOPK_MAX_K) return 0;
+        pq_index_s t = subset_index(idx, nV, nullptr, nullptr);
+        return subset_codes_bytes(idx, nV) + topk_ws(&t, B, K).total;
+    } catch (const pq::Error& e) {
+        set_error(e.msg);
+        return 0;
+    }
+}
+
+pq_status pq_score_topk_subset(pq_index idx, const float* S, int32_t B, int32_t K, const int32_t* V,
+                               int64_t nV, void* ws, size_t ws_bytes, int32_t* ids, float* scores,
+                               void* stream) {
+    PQ_API_BEGIN
+    need(idx != nullptr, "index is NULL");
+    check_topk_args(B, K);
+    need(nV >= 0, "nV must be >= 0");
+    if (B == 0 || K == 0) return PQ_OK;
+    need(S && ids && scores, "NULL pointer");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (nV == 0) {                                     // empty subset: all padding (R11)
+        std::vector<int32_t> hi((size_t)B * K, -1);
+        std::vector<float> hs((size_t)B * K, -INFINITY);
+        PQ_CUDA(cudaMemcpyAsync(ids, hi.data(), hi.size() * 4, cudaMemcpyHostToDevice, st));
+        PQ_CUDA(cudaMemcpyAsync(scores, hs.data(), hs.size() * 4, cudaMemcpyHostToDevice, st));
+        PQ_CUDA(cudaStreamSynchronize(st));
+        return PQ_OK;
+    }
+    need(V != nullptr && is_device_ptr(V), "V must be a device array of nV item ids");
+    const size_t nb = pq_subset_workspace_bytes(idx, nV, B, K);
+    if (!ws || ws_bytes < nb) fail(PQ_ERR_WORKSPACE, "workspace too small: need " + std::to_string(nb) + " bytes");
+    Carve c(ws);
+    uint8_t* codesV = c.take<uint8_t>((size_t)nV * idx->lay.mp + 64);
+    unsigned long long* bad = c.take<unsigned long long>(8);
+    PQ_CUDA(cudaMemsetAsync(bad, 0xFF, 8, st));
+    launch_check_subset(V, nV, idx->N, bad, st);
+    unsigned long long hbad = 0;
+    PQ_CUDA(cudaMemcpyAsync(&hbad, bad, 8, cudaMemcpyDeviceToHost, st));
+    PQ_CUDA(cudaStreamSynchronize(st));
+    if (hbad != ~0ull)
+        fail(PQ_ERR_INVALID_ARG, "V must hold strictly increasing local item ids in [0, N): first bad "
+                                 "position " + std::to_string(hbad));
+    launch_gather_codes(idx->d_codes, idx->lay.mp, V, nV, codesV, st);
+    pq_index_s t = subset_index(idx, nV, codesV, V);
+    run_score_topk(&t, S, B, K, c.base + c.off, ws_bytes - c.off, ids, scores, st);
+    PQ_API_END
+}
+
+size_t pq_exclude_workspace_bytes(pq_index idx, int32_t B, int32_t K, int32_t max_excl) {
+    try {
+        if (!idx || B <= 0 || K <= 0 || max_excl < 0 || K + max_excl > PQTOPK_MAX_K) return 0;
+        const int K2 = K + max_excl;
+        return 2 * align_up((size_t)B * K2 * 4, 256) + topk_ws(idx, B, K2).total;
+    } catch (const pq::Error& e) {
+        set_error(e.msg);
+        return 0;
+    }
+}
+
+pq_status pq_score_topk_exclude(pq_index idx, const float* S, int32_t B, int32_t K, const int32_t* excl,
+                                const int64_t* excl_off, int32_t max_excl, void* ws, size_t ws_bytes,
+                                int32_t* ids, float* scores, void* stream) {
+    PQ_API_BEGIN
+    need(idx != nullptr, "index is NULL");
+    check_topk_args(B, K);
+    need(max_excl >= 0, "max_excl must be >= 0");
+    if (K + max_excl > PQTOPK_MAX_K) fail(PQ_ERR_UNSUPPORTED, "K + max_excl exceeds PQTOPK_MAX_K (4096)");
+    if (B == 0 || K == 0) return PQ_OK;
+    need(S && ids && scores && excl_off, "NULL pointer");
+    need(max_excl == 0 || excl != nullptr, "excl is NULL");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const size_t nb = pq_exclude_workspace_bytes(idx, B, K, max_excl);
+    if (!ws || ws_bytes < nb) fail(PQ_ERR_WORKSPACE, "workspace too small: need " + std::to_string(nb) + " bytes");
+    const int K2 = K + max_excl;
+    Carve c(ws);
+    int32_t* ids2 = c.take<int32_t>((size_t)B * K2 * 4);
+    float* sc2 = c.take<float>((size_t)B * K2 * 4);
+    run_score_topk(idx, S, B, K2, c.base + c.off, ws_bytes - c.off, ids2, sc2, st);
+    launch_exclude(ids2, sc2, B, K2, excl, excl_off, K, ids, scores, st);
     PQ_API_END
 }
 

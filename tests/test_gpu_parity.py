@@ -365,3 +365,53 @@ def test_latency_parity(pq, torch, orc, case):
         idx.set_tuning(**tun)
         i, s = pq.pq_score_topk(idx, S_t, K)
         assert_same(i.cpu().numpy(), s.cpu().numpy(), *ref, str(tun))
+
+
+SUBSET_CASES = [
+    # seed, N, m, b, B, K, nV, dist
+    (600, 100_000, 8, 256, 3, 10, 5_000, "uniform"),      # small batch (v4 + row map)
+    (601, 80_001, 16, 256, 20, 100, 30_011, "uniform"),   # batched (v1 + row map)
+    (602, 50_000, 4, 16, 7, 300, 777, "few"),             # ties, K close to nV
+    (603, 20_000, 8, 256, 2, 50, 17, "uniform"),          # K > nV: padding
+]
+
+
+@pytest.mark.parametrize("case", SUBSET_CASES, ids=[str(c[0]) for c in SUBSET_CASES])
+def test_subset_parity(pq, torch, orc, case):
+    """Alg. 1 with an explicit item subset V: equals the oracle over
+    V, i.e. the full ranking restricted to V ("subset consistency")."""
+    seed, N, m, b, B, K, nV, dist = case
+    G, P, F = pqsynth.random_instance(seed, N, m, b, 4 * m, B, code_dist=dist)
+    rng = np.random.default_rng(seed)
+    V = np.sort(rng.choice(N, nV, replace=False)).astype(np.int32)
+    base = 1000 + seed
+    idx = pq.pq_create(G, b=b, id_base=base)
+    S_t = pq.pq_subscores(cuda(torch, F), cuda(torch, P))
+    ids, sc = pq.pq_score_topk_subset(idx, S_t, K, torch.from_numpy(V).cuda())
+    ri, rs = orc.pq_topk(G[V], S_t.cpu().numpy(), K)          # V ascending: row order = id order
+    ri = np.where(ri >= 0, V[np.clip(ri, 0, None)] + base, -1).astype(np.int32)
+    assert_same(ids.cpu().numpy(), sc.cpu().numpy(), ri, rs)
+    with pytest.raises(pq.PQError):                            # V must be strictly increasing
+        pq.pq_score_topk_subset(idx, S_t, K, torch.from_numpy(V[::-1].copy()).cuda())
+
+
+@pytest.mark.parametrize("B,K,dist", [(2, 10, "uniform"), (24, 100, "uniform"), (5, 64, "few")])
+def test_exclude_parity(pq, torch, orc, B, K, dist):
+    """V_u = I minus user u's exclusion list: equals the oracle over V_u."""
+    N, m, b = 60_007, 8, 256
+    G, P, F = pqsynth.random_instance(700 + B, N, m, b, 32, B, code_dist=dist)
+    idx = pq.pq_create(G, b=b, id_base=11)
+    S_t = pq.pq_subscores(cuda(torch, F), cuda(torch, P))
+    S_h = S_t.cpu().numpy()
+    full_i, _ = orc.pq_topk(G, S_h, 2 * K, id_base=11)
+    rng = np.random.default_rng(B)
+    excl = []
+    for u in range(B):        # drop some of the user's own best items plus random ones
+        own = full_i[u][rng.random(2 * K) < 0.4]
+        excl.append(np.concatenate([own, rng.integers(11, 11 + N, 20)]))
+    ids, sc = pq.pq_score_topk_exclude(idx, S_t, K, excl)
+    for u in range(B):
+        keep = np.setdiff1d(np.arange(N), np.asarray(excl[u]) - 11).astype(np.int32)
+        ri, rs = orc.pq_topk(G[keep], S_h[u:u + 1], K)
+        ri = np.where(ri >= 0, keep[np.clip(ri, 0, None)] + 11, -1).astype(np.int32)
+        assert_same(ids.cpu().numpy()[u:u + 1], sc.cpu().numpy()[u:u + 1], ri, rs, str(u))
