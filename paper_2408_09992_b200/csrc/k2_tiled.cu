@@ -73,6 +73,7 @@ struct K2TArgs {
     unsigned long long* gtau;  // [n_groups * R] per-user proved thresholds (zeroed per call)
     long long* trace;          // diagnostics (PQTOPK_K2_TRACE): CTA 0 phase timeline, or null
     int trace_stride;          // trace every trace_stride-th tile (PQTOPK_K2_TRACE_STRIDE)
+    int trace_from;            // first traced tile of CTA 0 (PQTOPK_K2_TRACE_FROM)
     int* dbg;                  // diagnostics (PQTOPK_K2_DEBUG): bounded spins record state here
 };
 constexpr int TRACE_PH = 256;  // traced table uses (CTA 0): [W][TRACE_PH][3]; then CTA 0 units [TRACE_PH/2][2];
@@ -263,6 +264,9 @@ __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
     int* tiles_done = done + NB;                       // [W] tiles finished by each warp
     int* sflag = tiles_done + W;                       // [2] shrink request: tile index + 1
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sflag + 2);
+    constexpr int LM = RPS * W;                        // lanes per user in the CTA
+    uint64_t* lmk = reinterpret_cast<uint64_t*>(sm_raw + align_up((size_t)(reinterpret_cast<char*>(tmem_slot + 4) -
+                                                                  reinterpret_cast<char*>(sm_raw)), 16));
     const uint32_t tbl0 = smem_u32(sm_raw);
     const uint32_t bar0 = smem_u32(mbar);
 
@@ -366,13 +370,77 @@ __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
         for (int j = 0; j < 4; ++j)
             tf[j] = (4 * q + j < n_valid) ? tau_to_filter(tau_sh[4 * q + j]) : INFINITY;
 
+        // Threshold seeding (single-phase tables, no threshold known yet): one
+        // extra pass over the unit's first tile computes, per user, each lane's
+        // best score; the K-th largest of those LM lane maxima (distinct items)
+        // proves a score floor, so the real first pass inserts ~K candidates
+        // per user instead of the whole tile (which would then need a costly
+        // shrink).
+        bool seeded = false;
+        if constexpr (NP == 1) {
+            bool any_unset = false;
+            for (int u = 0; u < n_valid; ++u) any_unset |= tau_sh[u] == 0ull;
+            if (any_unset && a.K <= LM) {
+                mbar_wait(bar0, (uint32_t)(useq & 1));
+                const char* tb = reinterpret_cast<const char*>(sm_raw);
+                const int64_t tile = tile0;
+                const char* cp = reinterpret_cast<const char*>(a.codes) +
+                                 (tile * TR + ((int64_t)warp * SL * RPS + (lane / LPR) * 2)) * CB;
+                const uint32_t row0 = (uint32_t)(tile * TR) + (uint32_t)(warp * SL * RPS) + (uint32_t)(lane / LPR);
+                float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+                bool got = false;
+#pragma unroll 1
+                for (int s2 = 0; s2 < SL; s2 += 2) {
+                    CodePair<PS> cpair;
+                    cpair.load(cp + (int64_t)(s2 / 2) * 2 * RPS * CB);
+#pragma unroll
+                    for (int e = 0; e < 2; ++e) {
+                        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+                        for (int kk = 0; kk < PS; ++kk) {
+                            const uint32_t w = cpair.w[e * (PS / 2) + (kk >> 1)];
+                            const uint32_t off = (kk & 1) ? hi16_add(w, q16) : ((w & 0xFFFFu) | q16);
+                            const float4 v = lds128(tb + kk * SPLITB + off);
+                            if (kk == 0) acc = v; else add4(acc, v);
+                        }
+                        if (a.perm[row0 + (uint32_t)(s2 + e) * RPS] >= 0) {
+                            got = true;
+                            mx[0] = fmaxf(mx[0], acc.x); mx[1] = fmaxf(mx[1], acc.y);
+                            mx[2] = fmaxf(mx[2], acc.z); mx[3] = fmaxf(mx[3], acc.w);
+                        }
+                    }
+                }
+                const int li = warp * RPS + lane / LPR;
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const float v = mx[j] + 0.0f;
+                    const uint32_t ub = __float_as_uint(v);
+                    const uint32_t o = (ub & 0x80000000u) ? ~ub : (ub | 0x80000000u);
+                    lmk[(4 * q + j) * LM + li] = got ? (((uint64_t)o << 32) | (uint32_t)(li + 1)) : 0ull;
+                }
+                __syncthreads();
+                for (int u = warp; u < n_valid; u += W) {
+                    if (tau_sh[u] != 0ull) continue;
+                    const uint64_t kth = warp_kth(lmk + u * LM, LM, (uint32_t)a.K, hist);
+                    // K distinct items score >= kth's score: floor = that score, any id
+                    if (lane == 0 && kth != 0ull) tau_sh[u] = kth & 0xFFFFFFFF00000000ull;
+                }
+                __syncthreads();
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    if (tf[j] != INFINITY) tf[j] = fmaxf(tf[j], tau_to_filter(tau_sh[4 * q + j]));
+                seeded = true;
+            }
+        }
+
         for (int64_t t = 0; t < ntl; ++t) {
             const int64_t tile = tile0 + t;
 #pragma unroll
             for (int ph = 0; ph < NP; ++ph) {
                 const int buf = NP > 1 ? ph % NB : 0;
                 const uint32_t par = NP > 1 ? (uint32_t)((gseq / NB) & 1) : (uint32_t)(useq & 1);
-                const int64_t tix = (tseq % a.trace_stride == 0) ? (tseq / a.trace_stride) * NP + ph : TRACE_PH;
+                const int64_t tq = tseq - a.trace_from;
+                const int64_t tix = (tq >= 0 && tq % a.trace_stride == 0) ? (tq / a.trace_stride) * NP + ph : TRACE_PH;
                 const bool trc = a.trace && blockIdx.x == 0 && lane == 0 && tix < TRACE_PH;
                 if (trc) a.trace[((int64_t)warp * TRACE_PH + tix) * 3 + 0] = clock64();
                 mbar_wait(bar0 + 8u * buf, par);
@@ -501,7 +569,7 @@ __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
             __threadfence_block();
             // (always after a unit's first tile: it ran with the unit's initial,
             // usually weak, thresholds)
-            const bool need = t == 0 || (tseq > 0 &&
+            const bool need = (t == 0 && !seeded) || (tseq > 0 &&
                 *reinterpret_cast<volatile int*>(&sflag[(tseq - 1) & 1]) == (int)tseq);
             if (need) {                                // uniform across the CTA
                 __syncthreads();                       // every insert so far is visible
@@ -625,8 +693,10 @@ int k2_tiled_rows_per_tile(int R) { return R == 32 ? 2048 : 4096; }
 size_t k2_tiled_smem(int m, int b, int R, int W) {
     const int ps = k2_tiled_ps(m);
     const int nb = (m / ps) > 1 ? 2 : 1;
-    return (size_t)nb * ps * b * R * 4 + (size_t)W * 1024 + (size_t)R * 8 + (size_t)R * 8 +
-           3 * 8 + 3 * 4 + (size_t)(W + 2) * 4 + 16;
+    const size_t base = (size_t)nb * ps * b * R * 4 + (size_t)W * 1024 + (size_t)R * 8 + (size_t)R * 8 +
+                        3 * 8 + 3 * 4 + (size_t)(W + 2) * 4 + 16;
+    const size_t lm = nb == 1 ? (size_t)R * (32 / (R / 4)) * W * 8 : 0;   // threshold seeding keys
+    return align_up(base, 16) + lm + 16;
 }
 
 // Item chunks per user group.  Units (group x chunk) are dealt round-robin to
@@ -720,6 +790,8 @@ void launch_k2_tiled(const pq_index_s* idx, const K2Plan& p, int B, int K,
     const char* tf = getenv("PQTOPK_K2_TRACE");
     const char* tsd = getenv("PQTOPK_K2_TRACE_STRIDE");
     a.trace_stride = tsd ? std::max(1, atoi(tsd)) : 1;
+    const char* tfr = getenv("PQTOPK_K2_TRACE_FROM");
+    a.trace_from = tfr ? std::max(0, atoi(tfr)) : 0;
     const size_t tn = (size_t)p.W * TRACE_PH * 3 + TRACE_PH + 3 * TRACE_CTAS;
     if (tf && *tf) {
         PQ_CUDA(cudaMalloc(&a.trace, tn * 8));
