@@ -143,10 +143,15 @@ __device__ __forceinline__ float tau_to_filter(uint64_t t) {
 template <int PS> struct CodePair {
     uint32_t w[PS];
     __device__ __forceinline__ void load(const char* p) {
+        if constexpr (PS == 2) {
+            const uint2 t = __ldg(reinterpret_cast<const uint2*>(p));
+            w[0] = t.x; w[1] = t.y;
+        } else {
 #pragma unroll
-        for (int x = 0; x < PS; x += 4) {
-            const uint4 t = __ldg(reinterpret_cast<const uint4*>(p) + x / 4);
-            w[x] = t.x; w[x + 1] = t.y; w[x + 2] = t.z; w[x + 3] = t.w;
+            for (int x = 0; x < PS; x += 4) {
+                const uint4 t = __ldg(reinterpret_cast<const uint4*>(p) + x / 4);
+                w[x] = t.x; w[x + 1] = t.y; w[x + 2] = t.z; w[x + 3] = t.w;
+            }
         }
     }
 };
@@ -663,12 +668,12 @@ typedef void (*K2TFn)(const K2TArgs);
 
 template <int M, int PS, int BT, int R>
 static K2TFn tiled_fn_w(int W) {
-    if (W == 32) return k2_tiled<M, PS, BT, R, 32, 2>;
     if (W == 16) return k2_tiled<M, PS, BT, R, 16, 4>;
     return k2_tiled<M, PS, BT, R, 8, 4>;
 }
 // Instantiated shapes: R = 16 (paired layout) for b = 256, m in {8, 16};
-// R = 32 (item order) when the 32-user table fits: (m, b) in {(4, 16), (8, 16), (4, 256)}.
+// R = 32 (item order) when the 32-user table fits: (m, b) in {(4, 16), (8, 16), (4, 256)},
+// and, in phases of 2 splits, b = 256 with m in {32, 64}.
 static K2TFn tiled_fn(int m, int b, int R, int W) {
     if (R == 16 && b == 256) {
         if (m == 16) return tiled_fn_w<16, 4, 256, 16>(W);
@@ -679,9 +684,12 @@ static K2TFn tiled_fn(int m, int b, int R, int W) {
         if (m == 8) return tiled_fn_w<8, 8, 16, 32>(W);
     }
     if (R == 32 && b == 256 && m == 4) return tiled_fn_w<4, 4, 256, 32>(W);
+    // many splits (Fig. 2b's m = 64): 32 users, phases of 2 splits (64 KB tables)
+    if (R == 32 && b == 256 && m == 32) return tiled_fn_w<32, 2, 256, 32>(W);
+    if (R == 32 && b == 256 && m == 64) return tiled_fn_w<64, 2, 256, 32>(W);
     return nullptr;
 }
-int k2_tiled_ps(int m) { return m == 16 ? 4 : m; }
+int k2_tiled_ps(int m) { return m == 16 ? 4 : (m >= 32 ? 2 : m); }
 int k2_tiled_users(int m, int b) {
     if (tiled_fn(m, b, 32, 16)) return 32;
     if (tiled_fn(m, b, 16, 16)) return 16;
@@ -722,7 +730,7 @@ void plan_k2_tiled(const pq_index_s* idx, int B, int K, K2Plan& p) {
     p.variant = 3;
     const pq_tuning& t = idx->tuning;
     const int R = idx->v3_R;
-    p.W = (t.warps == 8 || t.warps == 16 || t.warps == 32) ? t.warps : 16;
+    p.W = (t.warps == 8 || t.warps == 16) ? t.warps : 16;
     p.G = R; p.Ug = R; p.J = 1;
     p.tm = (idx->m / k2_tiled_ps(idx->m)) > 1 ? idx->m - k2_tiled_ps(idx->m) : 0;
     p.n_groups = (int)ceil_div(B, R);

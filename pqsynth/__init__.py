@@ -64,6 +64,8 @@ CONFIGS = {
                  note="Zipf(1.1) codes per split"),
     "c4": Config("c4", 4, 50_000_000, 16, 256, 512, 1024, 100, gpus=(1, 2, 4, 8),
                  note="graded: 50M items, item-sharded 1/2/4/8 GPUs"),
+    "c6": Config("c6", 6, 10_000_000, 64, 256, 512, 256, 100,
+                 note="next row f2: m = 64 splits (Fig. 2b, PAPER.md:257), not a BASELINE config"),
     "c5": Config("c5", 5, 200_000_000, 4, 16, 64, 4096, 1000, gpus=(8,),
                  note="tie stress: 65,536 code tuples"),
 }

@@ -319,6 +319,8 @@ TILED_CASES = [
     (306, 300_001, 4, 16, 70, 1000, "uniform"),      # C5-like: massive exact ties, R = 32
     (307, 90_001, 8, 16, 33, 50, "uniform"),
     (308, 5_003, 4, 16, 40, 3000, "uniform"),        # K close to N, ties
+    (309, 60_001, 64, 256, 40, 100, "uniform"),      # m = 64 (Fig. 2b): R = 32, 32 phases of 2 splits
+    (310, 30_011, 32, 256, 33, 500, "zipf"),         # m = 32
 ]
 
 
