@@ -554,8 +554,11 @@ __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
             }
 
             // ---- end of tile T = tseq: shrink if requested during tile T - 1
+            // (no memory fence here: a fence would also wait for this warp's
+            // outstanding global loads; the only cross-warp data read without a
+            // barrier is sflag, fenced by its writer, and __syncwarp orders the
+            // writer lane before lane 0's tiles_done store)
             __syncwarp();
-            __threadfence_block();
             if (lane == 0) *reinterpret_cast<volatile int*>(&tiles_done[warp]) = (int)(tseq + 1);
             // wait until every warp has finished tile T - 1 (bounds the skew to one tile)
             for (long long spins = 0;; ++spins) {
@@ -571,7 +574,6 @@ __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
                     break;
                 }
             }
-            __threadfence_block();
             // (always after a unit's first tile: it ran with the unit's initial,
             // usually weak, thresholds)
             const bool need = (t == 0 && !seeded) || (tseq > 0 &&

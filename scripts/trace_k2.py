@@ -35,3 +35,13 @@ if len(ctas):
           f"median {(np.median(en)-t0n)/1e6:.3f} max {(en.max()-t0n)/1e6:.3f} ms; tiles/CTA min {tl.min()} max {tl.max()}")
     ns_per_tile = (en - st) / np.maximum(tl, 1)
     print(f"  ns per tile: mean {ns_per_tile.mean():.0f} min {ns_per_tile.min():.0f} max {ns_per_tile.max():.0f}")
+# per-warp gaps between a tile's last phase end and the next tile's first wait start
+NPh = int(sys.argv[3]) if len(sys.argv) > 3 else 4
+if n >= 2 * NPh:
+    gaps = []
+    for g in range(NPh - 1, n - 1, NPh):
+        if g + 1 < n:
+            gaps.append((ev[:, g + 1, 0] - ev[:, g, 2]).mean())
+    print(f"mean tile-boundary gap per warp (cycles): {np.mean(gaps):.0f}  (NP={NPh})")
+    ph_len = [(ev[:, p::NPh, 2] - ev[:, p::NPh, 1])[:, : n // NPh].mean() for p in range(NPh)]
+    print("mean phase length by phase:", " ".join(f"{x:.0f}" for x in ph_len))
