@@ -686,12 +686,13 @@ static K2TFn tiled_fn(int m, int b, int R, int W) {
         if (m == 8) return tiled_fn_w<8, 8, 16, 32>(W);
     }
     if (R == 32 && b == 256 && m == 4) return tiled_fn_w<4, 4, 256, 32>(W);
-    // many splits (Fig. 2b's m = 64): 32 users, phases of 2 splits (64 KB tables)
-    if (R == 32 && b == 256 && m == 32) return tiled_fn_w<32, 2, 256, 32>(W);
-    if (R == 32 && b == 256 && m == 64) return tiled_fn_w<64, 2, 256, 32>(W);
+    // many splits (Fig. 2b's m = 64): 16 users in item order (no colour pairing:
+    // 64-split signatures have no complements), phases of 4 splits
+    if (R == 16 && b == 256 && m == 32) return tiled_fn_w<32, 4, 256, 16>(W);
+    if (R == 16 && b == 256 && m == 64) return tiled_fn_w<64, 4, 256, 16>(W);
     return nullptr;
 }
-int k2_tiled_ps(int m) { return m == 16 ? 4 : (m >= 32 ? 2 : m); }
+int k2_tiled_ps(int m) { return m >= 16 ? 4 : m; }
 int k2_tiled_users(int m, int b) {
     if (tiled_fn(m, b, 32, 16)) return 32;
     if (tiled_fn(m, b, 16, 16)) return 16;

@@ -187,9 +187,9 @@ static void build_v3_layout(pq_index_s* idx, const uint8_t* codes_in, const uint
         hc = hbuf.data();
     }
     PairLayout L;
-    if (R == 16) {
+    if (R == 16 && m <= 20) {
         L = build_pairing(hc, N, m, b, 0);
-    } else {
+    } else {                                           // item order, codes * (R * 4)
         L.rows = N;
         L.perm.resize((size_t)N);
         L.codes16.resize((size_t)N * m);
@@ -198,7 +198,7 @@ static void build_v3_layout(pq_index_s* idx, const uint8_t* codes_in, const uint
             for (int g = 0; g < b; ++g) L.cmap[(size_t)k * b + g] = (uint8_t)g;
         for (int64_t i = 0; i < N; ++i) {
             L.perm[(size_t)i] = (int32_t)i;
-            for (int k = 0; k < m; ++k) L.codes16[(size_t)i * m + k] = (uint16_t)(hc[i * m + k] * 128u);
+            for (int k = 0; k < m; ++k) L.codes16[(size_t)i * m + k] = (uint16_t)(hc[i * m + k] * (uint32_t)(R * 4));
         }
     }
     const int64_t TR = k2_tiled_rows_per_tile(R);
