@@ -133,7 +133,39 @@ static int64_t dense_lists(int64_t N, int64_t nc) {
 
 // K2 v2 layout (pairing.cu) when the shape is supported: b = 256, m in {4, 8, 16},
 // 16 users' tables in shared memory, or all but two splits (+2 in TMEM).
-static void build_v2_layout(pq_index_s* idx, const uint8_t* codes_in, const uint8_t* dev_src,
+// Host-side state shared by the layout builders of one pq_create: the codes
+// on the host (copied once if the caller passed device memory) and the colour
+// pairing (built once, used by the v2 and v3 layouts).
+struct CreateCtx {
+    std::vector<uint8_t> hbuf;
+    const uint8_t* hc = nullptr;
+    bool have_pair = false;
+    PairLayout pair0;                                  // pairing with every split in shared memory
+};
+static const uint8_t* host_codes(CreateCtx& cx, const pq_index_s* idx, const uint8_t* codes_in,
+                                 const uint8_t* dev_src, cudaStream_t st) {
+    if (!cx.hc) {
+        if (is_device_ptr(codes_in)) {
+            cx.hbuf.resize((size_t)idx->N * idx->m);
+            PQ_CUDA(cudaMemcpyAsync(cx.hbuf.data(), dev_src, cx.hbuf.size(), cudaMemcpyDeviceToHost, st));
+            PQ_CUDA(cudaStreamSynchronize(st));
+            cx.hc = cx.hbuf.data();
+        } else {
+            cx.hc = codes_in;
+        }
+    }
+    return cx.hc;
+}
+static const PairLayout& pairing0(CreateCtx& cx, const pq_index_s* idx, const uint8_t* codes_in,
+                                  const uint8_t* dev_src, cudaStream_t st) {
+    if (!cx.have_pair) {
+        cx.pair0 = build_pairing(host_codes(cx, idx, codes_in, dev_src, st), idx->N, idx->m, idx->b, 0);
+        cx.have_pair = true;
+    }
+    return cx.pair0;
+}
+
+static void build_v2_layout(pq_index_s* idx, CreateCtx& cx, const uint8_t* codes_in, const uint8_t* dev_src,
                             cudaStream_t st) {
     const int m = idx->m, b = idx->b;
     const size_t budget = idx->smem_optin;
@@ -141,16 +173,20 @@ static void build_v2_layout(pq_index_s* idx, const uint8_t* codes_in, const uint
     if (k2_paired_supported(m, 0, b) && k2_paired_smem(m, 0, b, 8) <= budget) tm = 0;
     else if (k2_paired_supported(m, 2, b) && k2_paired_smem(m, 2, b, 8) <= budget) tm = 2;
     if (tm < 0) return;
-    const int64_t N = idx->N;
-    std::vector<uint8_t> hbuf;
-    const uint8_t* hc = codes_in;
-    if (is_device_ptr(codes_in)) {
-        hbuf.resize((size_t)N * m);
-        PQ_CUDA(cudaMemcpyAsync(hbuf.data(), dev_src, (size_t)N * m, cudaMemcpyDeviceToHost, st));
-        PQ_CUDA(cudaStreamSynchronize(st));
-        hc = hbuf.data();
+    const PairLayout& L = pairing0(cx, idx, codes_in, dev_src, st);
+    // v2 stores the last tm splits as TMEM columns (stored code + b * t) instead of row offsets
+    std::vector<uint16_t> tcodes;
+    const uint16_t* codes16 = L.codes16.data();
+    if (tm > 0) {
+        tcodes = L.codes16;
+        const int ms = m - tm;
+        for (int64_t r = 0; r < L.rows; ++r)
+            for (int k = ms; k < m; ++k) {
+                uint16_t& c = tcodes[(size_t)r * m + k];
+                c = (uint16_t)(c / 64u + (uint32_t)b * (uint32_t)(k - ms));
+            }
+        codes16 = tcodes.data();
     }
-    PairLayout L = build_pairing(hc, N, m, b, tm);
     const size_t cbytes = (size_t)(L.rows + V2_PAD_ROWS) * m * 2;
     PQ_CUDA(cudaMalloc(&idx->d_codes16, cbytes));
     PQ_CUDA(cudaMalloc(&idx->d_perm16, (size_t)L.rows * 4));
@@ -158,7 +194,7 @@ static void build_v2_layout(pq_index_s* idx, const uint8_t* codes_in, const uint
     PQ_CUDA(cudaMalloc(&idx->d_pos16, (size_t)m * b));
     PQ_CUDA(cudaMemcpyAsync(idx->d_pos16, L.pos.data(), (size_t)m * b, cudaMemcpyHostToDevice, st));
     PQ_CUDA(cudaMemsetAsync(idx->d_codes16, 0, cbytes, st));
-    PQ_CUDA(cudaMemcpyAsync(idx->d_codes16, L.codes16.data(), (size_t)L.rows * m * 2, cudaMemcpyHostToDevice, st));
+    PQ_CUDA(cudaMemcpyAsync(idx->d_codes16, codes16, (size_t)L.rows * m * 2, cudaMemcpyHostToDevice, st));
     PQ_CUDA(cudaMemcpyAsync(idx->d_perm16, L.perm.data(), (size_t)L.rows * 4, cudaMemcpyHostToDevice, st));
     PQ_CUDA(cudaMemcpyAsync(idx->d_cmap16, L.cmap.data(), (size_t)m * b, cudaMemcpyHostToDevice, st));
     PQ_CUDA(cudaStreamSynchronize(st));
@@ -172,24 +208,19 @@ static void build_v2_layout(pq_index_s* idx, const uint8_t* codes_in, const uint
 // K2 v3 layout (k2_tiled.cu).  R = 16: the colour pairing (every split in
 // shared memory, stored codes * 64); R = 32: item order, codes * 128.  Rows are
 // padded to whole tiles and the codes phase-blocked ([tile][phase][row][PS]).
-static void build_v3_layout(pq_index_s* idx, const uint8_t* codes_in, const uint8_t* dev_src,
+static void build_v3_layout(pq_index_s* idx, CreateCtx& cx, const uint8_t* codes_in, const uint8_t* dev_src,
                             cudaStream_t st) {
     const int m = idx->m, b = idx->b;
     const int R = k2_tiled_users(m, b);
     if (!R || k2_tiled_smem(m, b, R, 16) > idx->smem_optin) return;
     const int64_t N = idx->N;
-    std::vector<uint8_t> hbuf;
-    const uint8_t* hc = codes_in;
-    if (is_device_ptr(codes_in)) {
-        hbuf.resize((size_t)N * m);
-        PQ_CUDA(cudaMemcpyAsync(hbuf.data(), dev_src, (size_t)N * m, cudaMemcpyDeviceToHost, st));
-        PQ_CUDA(cudaStreamSynchronize(st));
-        hc = hbuf.data();
-    }
-    PairLayout L;
+    const uint8_t* hc = host_codes(cx, idx, codes_in, dev_src, st);
+    PairLayout Lio;
+    const PairLayout* Lp = &Lio;
     if (R == 16 && m <= 20) {
-        L = build_pairing(hc, N, m, b, 0);
+        Lp = &pairing0(cx, idx, codes_in, dev_src, st);
     } else {                                           // item order, codes * (R * 4)
+        PairLayout& L = Lio;
         L.rows = N;
         L.perm.resize((size_t)N);
         L.codes16.resize((size_t)N * m);
@@ -201,6 +232,7 @@ static void build_v3_layout(pq_index_s* idx, const uint8_t* codes_in, const uint
             for (int k = 0; k < m; ++k) L.codes16[(size_t)i * m + k] = (uint16_t)(hc[i * m + k] * (uint32_t)(R * 4));
         }
     }
+    const PairLayout& L = *Lp;
     const int64_t TR = k2_tiled_rows_per_tile(R);
     const int64_t tiles = ceil_div(L.rows, TR);
     const int ps = k2_tiled_ps(m), np = m / ps;
@@ -314,8 +346,9 @@ pq_status pq_create(const uint8_t* codes, int64_t N, int32_t m, int32_t b, int64
                      (long long)(bad / m), (long long)(bad % m), (unsigned)v, b);
             fail(PQ_ERR_CODE_RANGE, msg);
         }
-        build_v2_layout(idx, codes, src, st);
-        build_v3_layout(idx, codes, src, st);
+        CreateCtx cx;
+        build_v2_layout(idx, cx, codes, src, st);
+        build_v3_layout(idx, cx, codes, src, st);
         if (tmp) { cudaFree(tmp); tmp = nullptr; }
         cudaFree(d_bad);
         d_bad = nullptr;
