@@ -58,8 +58,16 @@
 
 namespace pq {
 
+// Stored code width: 1 = the (colour-renumbered) sub-id byte, the kernel forms
+// the row offset (code * R * 4 | quad offset) with two integer ops; 2 = 16-bit
+// pre-shifted row offsets (one op, twice the code bytes).
+#ifndef K2_CODE_BYTES
+#define K2_CODE_BYTES 1
+#endif
+int k2_tiled_code_bytes() { return K2_CODE_BYTES; }
+
 struct K2TArgs {
-    const uint16_t* codes;     // phase-blocked pre-shifted codes (see above)
+    const void* codes;         // phase-blocked codes (see above), K2_CODE_BYTES each
     const int32_t* perm;       // [tiles * TR] row -> local id (-1 = padding)
     const float* St;           // [n_groups][m][b][R] tiled sub-score tables
     int64_t n_tiles;           // tiles in the catalogue
@@ -138,20 +146,34 @@ __device__ __forceinline__ float tau_to_filter(uint64_t t) {
 
 // Code words of one row for one phase and TWO consecutive slots: pq_create
 // interleaves slot pairs ([slot pair][row][2][PS] inside a phase block), so a
-// lane fetches both slots' PS 16-bit codes with 16-byte loads; words
-// [e * PS/2, (e+1) * PS/2) belong to slot parity e.
+// lane fetches both slots' PS codes with one or two vector loads.
 template <int PS> struct CodePair {
-    uint32_t w[PS];
+    static constexpr int BYTES = 2 * PS * K2_CODE_BYTES;     // per lane per slot pair
+    static constexpr int NW = BYTES / 4;
+    uint32_t w[NW];
     __device__ __forceinline__ void load(const char* p) {
-        if constexpr (PS == 2) {
+        if constexpr (NW == 1) {
+            w[0] = __ldg(reinterpret_cast<const uint32_t*>(p));
+        } else if constexpr (NW == 2) {
             const uint2 t = __ldg(reinterpret_cast<const uint2*>(p));
             w[0] = t.x; w[1] = t.y;
         } else {
 #pragma unroll
-            for (int x = 0; x < PS; x += 4) {
+            for (int x = 0; x < NW; x += 4) {
                 const uint4 t = __ldg(reinterpret_cast<const uint4*>(p) + x / 4);
                 w[x] = t.x; w[x + 1] = t.y; w[x + 2] = t.z; w[x + 3] = t.w;
             }
+        }
+    }
+    // byte offset of split kk's row for slot parity e, OR-ed with the quad offset
+    template <int RB>
+    __device__ __forceinline__ uint32_t off(int e, int kk, uint32_t q16) const {
+        if constexpr (K2_CODE_BYTES == 1) {
+            const uint32_t wd = w[(e * PS + kk) >> 2];
+            return ((wd >> (8 * ((e * PS + kk) & 3))) & 0xFFu) * RB + q16;
+        } else {
+            const uint32_t wd = w[(e * PS + kk) >> 1];
+            return ((e * PS + kk) & 1) ? ((wd >> 16) + q16) : ((wd & 0xFFFFu) | q16);
         }
     }
 };
@@ -250,7 +272,7 @@ __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
     constexpr uint32_t RB = R * 4;                     // bytes per table row
     constexpr uint32_t SPLITB = (uint32_t)BT * RB;     // bytes per split table
     constexpr uint32_t TBLB = (uint32_t)PS * SPLITB;   // bytes per table buffer
-    constexpr int CB = PS * 2;                         // code bytes per row per phase
+    constexpr int CB = PS * K2_CODE_BYTES;             // code bytes per row per phase
     static_assert(M % PS == 0, "phases");
     static_assert(SL % D == 0 && D % 2 == 0, "prefetch depth");
     static_assert(R == 16 || R == 32, "users per row");
@@ -403,8 +425,7 @@ __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
                         float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
                         for (int kk = 0; kk < PS; ++kk) {
-                            const uint32_t w = cpair.w[e * (PS / 2) + (kk >> 1)];
-                            const uint32_t off = (kk & 1) ? hi16_add(w, q16) : ((w & 0xFFFFu) | q16);
+                            const uint32_t off = cpair.template off<RB>(e, kk, q16);
                             const float4 v = lds128(tb + kk * SPLITB + off);
                             if (kk == 0) acc = v; else add4(acc, v);
                         }
@@ -473,10 +494,7 @@ __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
                         const int s = s0 + d;
                         uint32_t off[PS];              // row offsets | user-quad offset
 #pragma unroll
-                        for (int kk = 0; kk < PS; ++kk) {
-                            const uint32_t w = cw[d >> 1].w[(d & 1) * (PS / 2) + (kk >> 1)];
-                            off[kk] = (kk & 1) ? hi16_add(w, q16) : ((w & 0xFFFFu) | q16);
-                        }
+                        for (int kk = 0; kk < PS; ++kk) off[kk] = cw[d >> 1].template off<RB>(d & 1, kk, q16);
                         if (d & 1) {                   // both slots of the pair addressed: refill
                             cw[d >> 1].load(cp);       // DP pairs ahead (buffer is padded)
                             cp += PSTR;

@@ -236,7 +236,8 @@ static void build_v3_layout(pq_index_s* idx, CreateCtx& cx, const uint8_t* codes
     const int64_t TR = k2_tiled_rows_per_tile(R);
     const int64_t tiles = ceil_div(L.rows, TR);
     const int ps = k2_tiled_ps(m), np = m / ps;
-    std::vector<uint16_t> c3((size_t)tiles * TR * m, 0);
+    const int cb = k2_tiled_code_bytes();             // 1: sub-id byte, 2: pre-shifted row offset
+    std::vector<uint8_t> c3((size_t)tiles * TR * m * cb, 0);
     std::vector<int32_t> p3((size_t)tiles * TR, -1);
     // inside a phase block, slot pairs are interleaved: logical row rr = slot * RPS + r
     // is stored at ((slot / 2) * RPS + r) * 2 + slot % 2 (k2_tiled.cu, CodePair)
@@ -247,15 +248,19 @@ static void build_v3_layout(pq_index_s* idx, CreateCtx& cx, const uint8_t* codes
         const int64_t sr = ((gs >> 1) * RPS + ri) * 2 + (gs & 1);
         p3[(size_t)r] = L.perm[(size_t)r];
         for (int ph = 0; ph < np; ++ph)
-            for (int kk = 0; kk < ps; ++kk)
-                c3[(size_t)(((t * np + ph) * TR + sr) * ps + kk)] = L.codes16[(size_t)r * m + ph * ps + kk];
+            for (int kk = 0; kk < ps; ++kk) {
+                const uint16_t v = L.codes16[(size_t)r * m + ph * ps + kk];    // stored code * R * 4
+                const size_t at = (size_t)(((t * np + ph) * TR + sr) * ps + kk);
+                if (cb == 1) c3[at] = (uint8_t)(v / (uint32_t)(R * 4));
+                else reinterpret_cast<uint16_t*>(c3.data())[at] = v;
+            }
     }
-    const size_t cbytes = c3.size() * 2 + V3_CODE_PAD;
+    const size_t cbytes = c3.size() + V3_CODE_PAD;
     PQ_CUDA(cudaMalloc(&idx->d_codes3, cbytes));
     PQ_CUDA(cudaMalloc(&idx->d_perm3, p3.size() * 4));
     PQ_CUDA(cudaMalloc(&idx->d_cmap3, (size_t)m * b));
     PQ_CUDA(cudaMemsetAsync(idx->d_codes3, 0, cbytes, st));
-    PQ_CUDA(cudaMemcpyAsync(idx->d_codes3, c3.data(), c3.size() * 2, cudaMemcpyHostToDevice, st));
+    PQ_CUDA(cudaMemcpyAsync(idx->d_codes3, c3.data(), c3.size(), cudaMemcpyHostToDevice, st));
     PQ_CUDA(cudaMemcpyAsync(idx->d_perm3, p3.data(), p3.size() * 4, cudaMemcpyHostToDevice, st));
     PQ_CUDA(cudaMemcpyAsync(idx->d_cmap3, L.cmap.data(), (size_t)m * b, cudaMemcpyHostToDevice, st));
     PQ_CUDA(cudaStreamSynchronize(st));

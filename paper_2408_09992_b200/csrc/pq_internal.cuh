@@ -97,7 +97,7 @@ struct pq_index_s {
     int v3_R = 0;                  // users per table row (16: paired layout, 32: item order)
     int64_t v3_tiles = 0;          // tiles of k2_tiled_rows_per_tile(v3_R) rows
     int64_t v3_matched = 0, v3_leftover = 0;
-    uint16_t* d_codes3 = nullptr;  // [tiles][NP][4096][PS] pre-shifted stored codes (+ pad)
+    void* d_codes3 = nullptr;      // [tiles][NP][TR][PS] stored codes, k2_tiled_code_bytes() each (+ pad)
     int32_t* d_perm3 = nullptr;    // [tiles * 4096] row -> local id (-1 = padding)
     uint8_t* d_cmap3 = nullptr;    // [m][b] stored -> original
     pq_tuning tuning{};
@@ -140,6 +140,7 @@ void launch_k2_latency(const pq_index_s* idx, const K2Plan& p, const float* S, i
 // v3 helpers (k2_tiled.cu)
 bool k2_tiled_supported(int m, int b);
 int k2_tiled_users(int m, int b);
+int k2_tiled_code_bytes();
 int k2_tiled_ps(int m);
 int k2_tiled_rows_per_tile(int R);
 constexpr int V3_CODE_PAD = 4096;     // bytes after the last tile (prefetch overhang)
