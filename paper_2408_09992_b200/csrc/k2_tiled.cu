@@ -489,19 +489,30 @@ __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
                 for (int s0 = 0; s0 < SL; s0 += D) {
                     float4 accs[D];                    // last phase: candidate sums of the group
                     unsigned cmask = 0u;               // last phase: bit 4d+j = slot d, user 4q+j
+                    // software pipeline (single-phase tables): the gathers of slot
+                    // d + 1 are issued before the adds of slot d (two slots of loads
+                    // in flight); with TMEM phases the register budget favours one
+                    constexpr bool PIPE = (NP == 1);
+                    float4 vb[2][PS];
+                    auto gather = [&](int d, float4 (&dst)[PS]) {
 #pragma unroll
-                    for (int d = 0; d < D; ++d) {
-                        const int s = s0 + d;
-                        uint32_t off[PS];              // row offsets | user-quad offset
-#pragma unroll
-                        for (int kk = 0; kk < PS; ++kk) off[kk] = cw[d >> 1].template off<RB>(d & 1, kk, q16);
+                        for (int kk = 0; kk < PS; ++kk)
+                            dst[kk] = lds128(tb + kk * SPLITB + cw[d >> 1].template off<RB>(d & 1, kk, q16));
                         if (d & 1) {                   // both slots of the pair addressed: refill
                             cw[d >> 1].load(cp);       // DP pairs ahead (buffer is padded)
                             cp += PSTR;
                         }
-                        float4 v[PS];
+                    };
+                    if constexpr (PIPE) gather(0, vb[0]);
 #pragma unroll
-                        for (int kk = 0; kk < PS; ++kk) v[kk] = lds128(tb + kk * SPLITB + off[kk]);
+                    for (int d = 0; d < D; ++d) {
+                        const int s = s0 + d;
+                        if constexpr (PIPE) {
+                            if (d + 1 < D) gather(d + 1, vb[(d + 1) & 1]);
+                        } else {
+                            gather(d, vb[d & 1]);
+                        }
+                        float4 (&v)[PS] = vb[d & 1];
                         uint32_t tnxt[4];
                         if (ph > 0)                    // next slot's partials (the last slot re-reads its own)
                             tm_ld_issue(tcol0 + (uint32_t)min(s + 1, SL - 1) * 4u, tnxt);
