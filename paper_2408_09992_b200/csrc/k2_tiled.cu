@@ -177,26 +177,17 @@ template <int PS> struct CodePair {
         }
     }
 };
-__device__ __forceinline__ uint32_t hi16_add(uint32_t w, uint32_t add) {
-    uint32_t r;
-    asm("mad.hi.u32 %0, %1, 65536, %2;" : "=r"(r) : "r"(w), "r"(add));
-    return r;                                   // (w >> 16) + add
-}
 
 // Candidate entries.  The hot loop appends RAW entries (order-preserving score
 // bits << 32 | layout row) without touching the row -> item permutation, so the
 // slow path has no dependent global load; a buffer's raw tail [nconv, n) is
 // converted to ranking keys (score bits << 32 | ~global id, R3) in one batched
-// pass when the buffer is shrunk or merged.  Padding rows (perm = -1) become
+// pass (shrink_user) when the buffer is shrunk or merged.  Padding rows (perm = -1) become
 // key 0 ("empty") and are dropped.
 __device__ __forceinline__ uint64_t make_raw(float s, uint32_t row) {
     const uint32_t u = __float_as_uint(s);
     const uint32_t o = (u & 0x80000000u) ? ~u : (u | 0x80000000u);
     return ((uint64_t)o << 32) | row;
-}
-__device__ __forceinline__ uint64_t raw_to_key(uint64_t r, const int32_t* perm, uint32_t id_base) {
-    const int32_t lid = perm[(uint32_t)r];
-    return lid < 0 ? 0ull : ((r & 0xFFFFFFFF00000000ull) | (uint64_t)(0xFFFFFFFFu - (id_base + (uint32_t)lid)));
 }
 
 // Whole warp, one user: convert the raw tail, then keep only keys >= the K-th
