@@ -71,7 +71,9 @@ typedef struct {
     int32_t warps;       /* warps per CTA of the scoring kernel (0 = auto) */
     int32_t chunks;      /* item chunks per user group (0 = auto) */
     int32_t users_per_row; /* G, table row width in users (0 = auto; power of 2, <= 32) */
-    int32_t reserved[3];
+    int32_t shrink_watermark; /* K2 v3 candidate-buffer shrink watermark (0 = automatic; tests
+                                 use a small value to force frequent shrinks) */
+    int32_t reserved[2];
 } pq_tuning;
 
 /* ABI version, so a binding can refuse a mismatched library. */

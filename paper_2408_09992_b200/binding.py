@@ -43,7 +43,7 @@ class PQError(RuntimeError):
 class Tuning(ctypes.Structure):
     _fields_ = [("variant", ctypes.c_int32), ("ctas", ctypes.c_int32), ("warps", ctypes.c_int32),
                 ("chunks", ctypes.c_int32), ("users_per_row", ctypes.c_int32),
-                ("reserved", ctypes.c_int32 * 3)]
+                ("shrink_watermark", ctypes.c_int32), ("reserved", ctypes.c_int32 * 2)]
 
 
 def lib_path() -> str:
@@ -207,8 +207,8 @@ class PQIndex:
                 "tmem_splits", "smem_bytes"]
         return dict(zip(keys, [int(x) for x in out]))
 
-    def set_tuning(self, variant=0, ctas=0, warps=0, chunks=0, users_per_row=0):
-        t = Tuning(variant, ctas, warps, chunks, users_per_row)
+    def set_tuning(self, variant=0, ctas=0, warps=0, chunks=0, users_per_row=0, shrink_watermark=0):
+        t = Tuning(variant, ctas, warps, chunks, users_per_row, shrink_watermark)
         _check(load_library().pq_set_tuning(self._h, ctypes.byref(t)))
 
     def timing_enable(self, on: bool = True):

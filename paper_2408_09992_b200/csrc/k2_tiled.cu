@@ -77,6 +77,7 @@ struct K2TArgs {
     int64_t chunk_tiles;       // tiles per item chunk
     uint64_t* ubuf;            // [grid][R][cap] per-user candidate buffers
     int cap;                   // >= 2K + 2 TR + 96 (see the shrink protocol)
+    int wm;                    // shrink watermark (<= cap - 2 TR - 32)
     uint64_t* cand;            // [B][chunks][K]
     unsigned long long* gtau;  // [n_groups * R] per-user proved thresholds (zeroed per call)
     long long* trace;          // diagnostics (PQTOPK_K2_TRACE): CTA 0 phase timeline, or null
@@ -362,7 +363,7 @@ __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
     // the end of tile T + 1 every warp (having waited until all warps finished
     // tile T) sees the same flag and the CTA shrinks.  Between the request and
     // the shrink at most 2 * TR more entries arrive: cap >= wm + 2 * TR.
-    const int wm = a.cap - 2 * TR - 32;
+    const int wm = a.wm;
     int64_t tseq = 0;                                  // tiles done by this CTA
 
     constexpr int64_t PSTR = 2 * RPS * CB;             // code bytes per slot pair
@@ -812,6 +813,12 @@ void launch_k2_tiled(const pq_index_s* idx, const K2Plan& p, int B, int K,
     a.id_base = (uint32_t)idx->id_base;
     a.n_groups = p.n_groups; a.chunks = p.chunks; a.chunk_tiles = p.chunk_items;
     a.ubuf = lanebuf; a.cap = p.cap; a.cand = cand;
+    {
+        const int TR = k2_tiled_rows_per_tile(p.G);
+        const int wmax = p.cap - 2 * TR - 32;
+        const int tw = idx->tuning.shrink_watermark;
+        a.wm = tw > 0 ? std::min(std::max(tw, K + 1), wmax) : wmax;
+    }
     a.gtau = gtau_of(idx, p, St);
     const char* dbe = getenv("PQTOPK_K2_DEBUG");
     if (dbe && *dbe) {

@@ -439,6 +439,7 @@ pq_status pq_set_tuning(pq_index idx, const pq_tuning* t) {
         need(t->warps >= 0 && t->warps <= 32, "tuning.warps must be in [0, 32]");
         need(t->ctas >= 0 && t->chunks >= 0 && t->variant >= 0, "tuning values must be >= 0");
         need(t->users_per_row >= 0 && t->users_per_row <= 32, "tuning.users_per_row must be in [0, 32]");
+        need(t->shrink_watermark >= 0, "tuning.shrink_watermark must be >= 0");
         idx->tuning = *t;
     } else {
         idx->tuning = pq_tuning{};

@@ -335,7 +335,8 @@ def test_tiled_parity(pq, torch, orc, case):
     assert 3 in idx.variants()
     S_t = pq.pq_subscores(cuda(torch, F), cuda(torch, P))
     ref = orc.pq_topk(G, S_t.cpu().numpy(), K, id_base=seed)
-    for tun in (dict(variant=3), dict(variant=3, warps=8, ctas=3, chunks=5)):
+    for tun in (dict(variant=3), dict(variant=3, warps=8, ctas=3, chunks=5),
+                dict(variant=3, ctas=7, shrink_watermark=1)):       # shrink after almost every tile
         idx.set_tuning(**tun)
         assert idx.plan(B, K)["variant"] == 3
         i, s = pq.pq_score_topk(idx, S_t, K)
