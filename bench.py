@@ -218,7 +218,8 @@ def run_ours(args):
     F = pqsynth.phi(cfg)
 
     t0 = time.perf_counter()
-    idx = pq.pq_create(codes, b=b, id_base=lo)
+    # small-batch configs only need the item-order layout (skips host-side pairing)
+    idx = pq.pq_create(codes, b=b, id_base=lo, small_batch_only=B <= 4)
     torch.cuda.synchronize()
     create_s = time.perf_counter() - t0
     if args.variant or args.tuning:
@@ -372,21 +373,32 @@ def run_ours(args):
     tp = os.path.join(ROOT, "profiles", f"k2_traffic_{cfg.name}.json")
     if os.path.exists(tp):
         traffic = json.load(open(tp)).get("dram_bytes_per_launch")
-    roofline = {
-        "bound": "smem",
-        "kernel": {1: "k2_score_select (v1 row groups)", 2: "k2_paired (v2)",
-                   3: "k2_tiled (v3: fused gather-sum-select, 4 users/lane)"}.get(plan["variant"], "k2"),
-        "achieved": achieved / 1e9, "peak": peak_lookups / 1e9, "unit": "G lookups/s",
-        "frac": achieved / peak_lookups, "traffic": traffic,
-        "achieved_GBps_smem": achieved * 4 / 1e9, "peak_GBps_smem": peak_lookups * 4 / 1e9,
-        "peak_source": f"{nsm} SMs x 32 banks x 4 B x {f_max:.0f} MHz (sm_max_mhz, {pk['source']}); "
-                       "128 B/clk/SM attained by the paired LDS.128 pattern in the smem microbenchmark "
-                       "(profiles/r01/ubench/smem_rate_b200.txt)",
-        "per_launch": {"lookups": lookups, "algorithmic_hbm_bytes": n_local * m + B * m * b * 4 + B * K * 8,
-                       "k2_ms": k2_avg_s * 1e3},
+    # The binding roofline of the fused kernel: the shared-memory lookup rate
+    # (m lookups per user-item pair) or, for tiny batches, the HBM stream of
+    # the code matrix (m bytes per item, once per batch) -- whichever takes longer.
+    hbm_bytes = n_local * m + B * m * b * 4 + B * K * 8          # algorithmic bytes per launch
+    peak_hbm = pk["hbm_gbs"] * 1e9
+    t_smem, t_hbm = lookups / peak_lookups, hbm_bytes / peak_hbm
+    kname = {1: "k2_score_select (v1 row groups)", 2: "k2_paired (v2)",
+             3: "k2_tiled (v3: fused gather-sum-select, 4 users/lane)",
+             4: "k2_latency (v4: small-batch fused gather-sum-select)"}.get(plan["variant"], "k2")
+    common = {
+        "kernel": kname, "traffic": traffic,
+        "per_launch": {"lookups": lookups, "algorithmic_hbm_bytes": hbm_bytes, "k2_ms": k2_avg_s * 1e3},
         "k2_share_of_step": k2_avg_s * 1e3 / ms_per_step,
-        "hbm_frac_algorithmic": (n_local * m / k2_avg_s) / (pk["hbm_gbs"] * 1e9),
+        "smem_frac": achieved / peak_lookups,
+        "hbm_frac_algorithmic": (hbm_bytes / k2_avg_s) / peak_hbm,
+        "peak_source_smem": f"{nsm} SMs x 32 banks x 4 B x {f_max:.0f} MHz (sm_max_mhz, {pk['source']}); "
+                            "128 B/clk/SM attained by the paired LDS.128 pattern in the smem microbenchmark "
+                            "(profiles/r01/ubench/smem_rate_b200.txt)",
+        "peak_source_hbm": f"hbm_gbs {pk['hbm_gbs']} ({pk['source']})",
     }
+    if t_smem >= t_hbm:
+        roofline = {"bound": "smem", "achieved": achieved / 1e9, "peak": peak_lookups / 1e9,
+                    "unit": "G lookups/s", "frac": achieved / peak_lookups, **common}
+    else:
+        roofline = {"bound": "hbm", "achieved": hbm_bytes / k2_avg_s / 1e9, "peak": pk["hbm_gbs"],
+                    "unit": "GB/s", "frac": (hbm_bytes / k2_avg_s) / peak_hbm, **common}
     cpu = None
     parity = None
     if world == 1 and not args.no_cpu_baseline:

@@ -102,6 +102,15 @@ int64_t pq_launch_count(void);
 pq_status pq_create(const uint8_t* codes, int64_t N, int32_t m, int32_t b,
                     int64_t id_base, void* stream, pq_index* out);
 
+/* pq_create_ex — pq_create with flags:
+ *   PQ_CREATE_SMALL_BATCH_ONLY: build only the item-order layout (scoring
+ *     with B <= 4 and the generic kernel); skips the batched (paired / tiled)
+ *     layouts and their host-side colour pairing — for latency-serving
+ *     indexes and very large catalogues (e.g. 10^9 items). */
+#define PQ_CREATE_SMALL_BATCH_ONLY 1
+pq_status pq_create_ex(const uint8_t* codes, int64_t N, int32_t m, int32_t b,
+                       int64_t id_base, int32_t flags, void* stream, pq_index* out);
+
 /* Frees the index (synchronises the device first).  NULL is a no-op. */
 pq_status pq_destroy(pq_index idx);
 

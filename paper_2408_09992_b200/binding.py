@@ -24,7 +24,7 @@ PQ_STATUS = {0: "PQ_OK", 1: "PQ_ERR_INVALID_ARG", 2: "PQ_ERR_CODE_RANGE", 3: "PQ
              7: "PQ_ERR_WORKSPACE"}
 MAX_K = 4096
 
-EXPORTS = ["pq_abi_version", "pq_last_error", "pq_launch_count", "pq_create", "pq_destroy",
+EXPORTS = ["pq_abi_version", "pq_last_error", "pq_launch_count", "pq_create", "pq_create_ex", "pq_destroy",
            "pq_index_info", "pq_index_layout", "pq_index_variants", "pq_plan_info", "pq_set_tuning", "pq_subscores", "pq_topk_workspace_bytes",
            "pq_score_topk", "pq_search_workspace_bytes", "pq_search", "pq_merge_workspace_bytes",
            "pq_merge_topk", "pq_reconstruct", "pq_dense_workspace_bytes", "pq_dense_topk",
@@ -66,6 +66,7 @@ def load_library():
         "pq_last_error": (ctypes.c_char_p, []),
         "pq_launch_count": (I64, []),
         "pq_create": (st, [P, I64, I32, I32, I64, P, ctypes.POINTER(P)]),
+        "pq_create_ex": (st, [P, I64, I32, I32, I64, I32, P, ctypes.POINTER(P)]),
         "pq_destroy": (st, [P]),
         "pq_index_info": (st, [P, ctypes.POINTER(I64), ctypes.POINTER(I32), ctypes.POINTER(I32),
                                ctypes.POINTER(I64)]),
@@ -230,8 +231,12 @@ class PQIndex:
         return int(load_library().pq_recjpq_workspace_bytes(self._h, B, K))
 
 
-def pq_create(codes, b: int, id_base: int = 0, stream=None) -> PQIndex:
-    """Build an index from codes uint8 [N][m] (numpy / CPU tensor / CUDA tensor)."""
+SMALL_BATCH_ONLY = 1
+
+
+def pq_create(codes, b: int, id_base: int = 0, stream=None, small_batch_only: bool = False) -> PQIndex:
+    """Build an index from codes uint8 [N][m] (numpy / CPU tensor / CUDA tensor).
+    small_batch_only: skip the batched layouts (B <= 4 serving / huge catalogues)."""
     L = load_library()
     if isinstance(codes, np.ndarray):
         codes = np.ascontiguousarray(codes, dtype=np.uint8)
@@ -239,8 +244,9 @@ def pq_create(codes, b: int, id_base: int = 0, stream=None) -> PQIndex:
         codes = codes.contiguous()
     N, m = int(codes.shape[0]), int(codes.shape[1])
     h = ctypes.c_void_p()
-    _check(L.pq_create(ctypes.c_void_p(_ptr(codes)), N, m, int(b), int(id_base),
-                       ctypes.c_void_p(_stream(stream)), ctypes.byref(h)))
+    _check(L.pq_create_ex(ctypes.c_void_p(_ptr(codes)), N, m, int(b), int(id_base),
+                          SMALL_BATCH_ONLY if small_batch_only else 0,
+                          ctypes.c_void_p(_stream(stream)), ctypes.byref(h)))
     return PQIndex(h.value, N, m, int(b), int(id_base))
 
 

@@ -18,6 +18,7 @@
 // (user, item chunk) ends with its exact top-K list for K3.  Sum order as
 // everywhere: acc = S[0] + S[1] + ... + S[m-1] in fp32, +0.0f when keyed (R1/R2).
 #include "k2_common.cuh"
+#include "ptx_dev.cuh"
 
 namespace pq {
 
@@ -29,34 +30,63 @@ struct K2LArgs {
     int mp, b, B, K;
     uint32_t id_base;
     int chunks;
-    int64_t chunk_items;
+    int64_t chunk_items;       // multiple of 16 (16-byte aligned code stages)
     uint64_t* cand;            // [B][chunks][K]
+    int nst;                   // code stages in flight (TMA ring)
 };
 
 constexpr int K2L_THREADS = 256;
-constexpr int K2L_J = 4;                              // items per thread per round
-constexpr int K2L_CAP = 2 * K2L_THREADS * K2L_J;      // shared candidate buffer (keys)
+constexpr int K2L_STAGE = 16384;                      // code bytes per round (one TMA stage)
 
+// M splits (row = MP bytes), G table copies, NST code stages in flight.
 template <int M, int G>
 __global__ void __launch_bounds__(K2L_THREADS) k2_latency(const K2LArgs a) {
-    extern __shared__ __align__(16) unsigned char sm_raw[];
+    constexpr int MP = (M + 3) / 4 * 4;               // bytes per item row
+    constexpr int NW = MP / 4;                        // code words per row
+    constexpr int IPR = K2L_STAGE / MP;               // items per round
+    constexpr int J = IPR / K2L_THREADS;              // items per thread per round
+    constexpr int CAP = 2 * IPR;                      // shared candidate buffer (keys)
+    extern __shared__ __align__(128) unsigned char sm_raw[];
     float* T = reinterpret_cast<float*>(sm_raw);                      // [M][b][G]
-    uint64_t* cbuf = reinterpret_cast<uint64_t*>(sm_raw + align_up((size_t)M * a.b * G * 4, 16));
-    uint32_t* hist = reinterpret_cast<uint32_t*>(cbuf + K2L_CAP);     // [256]
+    unsigned char* ring = sm_raw + align_up((size_t)M * a.b * G * 4, 128);       // [nst][K2L_STAGE]
+    uint64_t* cbuf = reinterpret_cast<uint64_t*>(ring + (size_t)a.nst * K2L_STAGE);
+    uint32_t* hist = reinterpret_cast<uint32_t*>(cbuf + CAP);         // [256]
     __shared__ int count;
     __shared__ unsigned long long tau;
     __shared__ unsigned long long sc[4];
     __shared__ int wsum[K2L_THREADS / 32];
+    __shared__ __align__(8) unsigned long long mbar[8];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int rep = lane % G;
     const int64_t units = (int64_t)a.B * a.chunks;
+    const uint32_t bar0 = smem_u32(mbar), ring0 = smem_u32(ring);
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < a.nst; ++i) mbar_init(bar0 + 8u * i, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    int64_t g = 0;                                    // rounds consumed by this CTA (ring position)
 
     for (int64_t unit = blockIdx.x; unit < units; unit += gridDim.x) {
         const int u = (int)(unit % a.B);
         const int chunk = (int)(unit / a.B);
         const int64_t i0 = (int64_t)chunk * a.chunk_items;
         const int64_t i1 = min(a.N, i0 + a.chunk_items);
+        const int64_t rounds = (i1 - i0 + IPR - 1) / IPR;
         __syncthreads();
+        // stream this unit's code rows through the ring: the unit's round r is ring
+        // position g0 + r (slot (g0 + r) % nst), g0 = rounds consumed before the unit
+        const int64_t g0 = g;
+        auto issue = [&](int64_t r) {
+            const int slot = (int)((g0 + r) % a.nst);
+            const int64_t s0 = i0 + r * IPR;
+            const uint32_t bytes = (uint32_t)align_up((size_t)(min((int64_t)IPR, i1 - s0) * MP), 16);
+            const uint32_t bar = bar0 + 8u * slot;
+            fence_proxy_async();
+            mbar_expect_tx(bar, bytes);
+            bulk_g2s(ring0 + (uint32_t)slot * K2L_STAGE, a.codes + s0 * MP, bytes, bar);
+        };
+        if (threadIdx.x == 0)
+            for (int64_t r = 0; r < min((int64_t)a.nst, rounds); ++r) issue(r);
         {   // stage the user's table, G copies per row (rows loaded once, independent loads)
             const float* Su = a.S + (int64_t)u * M * a.b;
             const int rows = M * a.b;
@@ -87,39 +117,40 @@ __global__ void __launch_bounds__(K2L_THREADS) k2_latency(const K2LArgs a) {
         __syncthreads();
         float tf = -INFINITY;
         const float* Tl = T + rep;
-        constexpr int NW = (M + 3) / 4;                   // code words per item row
-        auto load_codes = [&](int64_t r0, uint32_t (&cw)[K2L_J][NW]) {
+
+        for (int64_t r = 0; r < rounds; ++r, ++g) {
+            const int slot = (int)(g % a.nst);
+            mbar_wait(bar0 + 8u * slot, (uint32_t)((g / a.nst) & 1));
+            const unsigned char* cs = ring + (size_t)slot * K2L_STAGE;
+            const int64_t r0 = i0 + r * IPR;
+            uint64_t keys[J];
 #pragma unroll
-            for (int j = 0; j < K2L_J; ++j) {
-                const int64_t item = r0 + (int64_t)j * K2L_THREADS + threadIdx.x;
-                const uint8_t* row = a.codes + (item < i1 ? item : i0) * a.mp;
-#pragma unroll
-                for (int q = 0; q < NW; ++q) cw[j][q] = __ldg(reinterpret_cast<const uint32_t*>(row) + q);
-            }
-        };
-        uint32_t cw[K2L_J][NW];
-        load_codes(i0, cw);
-        int round = 0;
-        for (int64_t r0 = i0; r0 < i1; r0 += (int64_t)K2L_THREADS * K2L_J, ++round) {
-            uint32_t nx[K2L_J][NW];                        // next round's codes (prefetch)
-            const int64_t r1 = r0 + (int64_t)K2L_THREADS * K2L_J;
-            if (r1 < i1) load_codes(r1, nx);
-            uint64_t keys[K2L_J];
-#pragma unroll
-            for (int j = 0; j < K2L_J; ++j) {
-                const int64_t item = r0 + (int64_t)j * K2L_THREADS + threadIdx.x;
-                float acc = Tl[(cw[j][0] & 0xFFu) * G];
+            for (int j = 0; j < J; ++j) {
+                const int li = j * K2L_THREADS + threadIdx.x;            // item within the round
+                const int64_t item = r0 + li;
+                uint32_t cw[NW];
+                if constexpr (NW == 1) {
+                    cw[0] = *reinterpret_cast<const uint32_t*>(cs + (size_t)li * MP);
+                } else if constexpr (NW == 2) {
+                    const uint2 t = *reinterpret_cast<const uint2*>(cs + (size_t)li * MP);
+                    cw[0] = t.x; cw[1] = t.y;
+                } else {
+                    const uint4 t = *reinterpret_cast<const uint4*>(cs + (size_t)li * MP);
+                    cw[0] = t.x; cw[1] = t.y; cw[2] = t.z; cw[3] = t.w;
+                }
+                float acc = Tl[(cw[0] & 0xFFu) * G];
 #pragma unroll
                 for (int k = 1; k < M; ++k) {
-                    const uint32_t g = (cw[j][k >> 2] >> (8 * (k & 3))) & 0xFFu;
-                    acc = acc + Tl[((size_t)k * a.b + g) * G];
+                    const uint32_t gk = (cw[k >> 2] >> (8 * (k & 3))) & 0xFFu;
+                    acc = acc + Tl[((size_t)k * a.b + gk) * G];
                 }
-                const uint32_t lid = (item < i1 && a.perm) ? (uint32_t)a.perm[item] : (uint32_t)item;
-                keys[j] = (item < i1 && acc >= tf) ? make_key(acc + 0.0f, a.id_base + lid) : 0ull;
+                const bool in = item < i1;
+                const uint32_t lid = (in && a.perm) ? (uint32_t)a.perm[item] : (uint32_t)item;
+                keys[j] = (in && acc >= tf) ? make_key(acc + 0.0f, a.id_base + lid) : 0ull;
             }
             // append this round's candidates (warp-aggregated slots)
 #pragma unroll
-            for (int j = 0; j < K2L_J; ++j) {
+            for (int j = 0; j < J; ++j) {
                 const bool c = keys[j] != 0ull && keys[j] > tau;
                 const unsigned bm = __ballot_sync(FULL, c);
                 if (bm) {
@@ -129,11 +160,12 @@ __global__ void __launch_bounds__(K2L_THREADS) k2_latency(const K2LArgs a) {
                     if (c) cbuf[base + __popc(bm & lanemask_lt())] = keys[j];
                 }
             }
-            __syncthreads();
+            __syncthreads();                               // every thread is done with this slot
+            if (threadIdx.x == 0 && r + a.nst < rounds) issue(r + a.nst);
             const int n_now = count;                       // same value in every thread
             // shrink after the first round (it ran without a threshold) and
             // whenever the next round could overflow the buffer
-            if (((round == 0 && r1 < i1) || n_now > K2L_CAP - K2L_THREADS * K2L_J) && n_now > a.K) {
+            if (((r == 0 && rounds > 1) || n_now > CAP - IPR) && n_now > a.K) {
                 const uint64_t kth = block_kth(cbuf, n_now, (uint32_t)a.K, hist, sc);
                 // compact in place: block-wide ballot prefix over chunks of blockDim
                 int base = 0;
@@ -155,12 +187,6 @@ __global__ void __launch_bounds__(K2L_THREADS) k2_latency(const K2LArgs a) {
             }
             __syncthreads();                               // nobody appends before all read count
             tf = tau ? key_score(tau) : -INFINITY;
-            if (r1 < i1) {
-#pragma unroll
-                for (int j = 0; j < K2L_J; ++j)
-#pragma unroll
-                    for (int q = 0; q < NW; ++q) cw[j][q] = nx[j][q];
-            }
         }
 
         // ---- end of unit: the unit's exact top-K list ---------------------
@@ -204,35 +230,40 @@ static K2LFn latency_fn(int m, int G) {
         default: return nullptr;
     }
 }
-static size_t latency_smem(int m, int b, int G) {
-    return align_up((size_t)m * b * G * 4, 16) + (size_t)K2L_CAP * 8 + 256 * 4;
+static int latency_mp(int m) { return (m + 3) / 4 * 4; }
+static size_t latency_smem(int m, int b, int G, int nst) {
+    const int ipr = K2L_STAGE / latency_mp(m);
+    return align_up((size_t)m * b * G * 4, 128) + (size_t)nst * K2L_STAGE + (size_t)2 * ipr * 8 + 256 * 4;
 }
 
 bool k2_latency_supported(const pq_index_s* idx, int B, int K) {
     return B >= 1 && B <= 4 && K <= 512 && latency_fn(idx->m, 1) != nullptr &&
-           latency_smem(idx->m, idx->b, 1) <= idx->smem_optin;
+           latency_smem(idx->m, idx->b, 1, 2) <= idx->smem_optin;
 }
 
 void plan_k2_latency(const pq_index_s* idx, int B, int K, K2Plan& p) {
     p.variant = 4;
     const pq_tuning& t = idx->tuning;
-    int G = 16;
-    while (G > 1 && latency_smem(idx->m, idx->b, G) > std::min<size_t>(idx->smem_optin, 200 * 1024)) G >>= 1;
-    p.G = G; p.Ug = 1; p.W = K2L_THREADS / 32; p.J = K2L_J; p.tm = 0;
+    // table copies (bank-conflict relief) first, then code stages in flight
+    int G = 16, nst = 4;
+    const size_t budget = idx->smem_optin;
+    while (G > 1 && latency_smem(idx->m, idx->b, G, 2) > budget) G >>= 1;
+    while (nst > 2 && latency_smem(idx->m, idx->b, G, nst) > budget) --nst;
+    p.G = G; p.Ug = 1; p.W = K2L_THREADS / 32; p.J = nst; p.tm = 0;
     p.n_groups = B;
-    p.smem = latency_smem(idx->m, idx->b, G);
+    p.smem = latency_smem(idx->m, idx->b, G, nst);
     K2LFn fn = latency_fn(idx->m, G);
     PQ_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem));
-    // chunks: about one wave of CTAs, >= one round (blockDim * J items) each
+    // chunks: about one wave of CTAs, >= one round each, 16-item aligned
     const int64_t N = idx->N;
-    const int64_t want = std::max<int64_t>(1, std::min<int64_t>(ceil_div(idx->num_sms, B),
-                                                               ceil_div(N, (int64_t)K2L_THREADS * K2L_J)));
+    const int64_t ipr = K2L_STAGE / latency_mp(idx->m);
+    const int64_t want = std::max<int64_t>(1, std::min<int64_t>(ceil_div(idx->num_sms, B), ceil_div(N, ipr)));
     p.chunks = t.chunks > 0 ? t.chunks : (int)want;
-    p.chunk_items = ceil_div(N, p.chunks);
+    p.chunk_items = (int64_t)align_up((size_t)ceil_div(N, p.chunks), 16);
     p.chunks = (int)ceil_div(N, p.chunk_items);
     const int64_t units = (int64_t)B * p.chunks;
     p.grid = (int)std::min<int64_t>(units, t.ctas > 0 ? t.ctas : (int64_t)idx->num_sms);
-    p.cap = K2L_CAP;
+    p.cap = 0;
     p.lanebuf_bytes = 0; p.mscr_bytes = 0; p.ghist_bytes = 0; p.st_bytes = 0;
     p.cand_bytes = (size_t)B * p.chunks * K * 8;
 }
@@ -248,6 +279,7 @@ void launch_k2_latency(const pq_index_s* idx, const K2Plan& p, const float* S, i
     a.id_base = (uint32_t)idx->id_base;
     a.chunks = p.chunks; a.chunk_items = p.chunk_items;
     a.cand = cand;
+    a.nst = p.J;
     K2LFn fn = latency_fn(idx->m, p.G);
     fn<<<p.grid, K2L_THREADS, p.smem, st>>>(a);
     count_launch();

@@ -297,6 +297,11 @@ int64_t pq_launch_count(void) { return g_launches.load(); }
 
 pq_status pq_create(const uint8_t* codes, int64_t N, int32_t m, int32_t b, int64_t id_base,
                     void* stream, pq_index* out) {
+    return pq_create_ex(codes, N, m, b, id_base, 0, stream, out);
+}
+
+pq_status pq_create_ex(const uint8_t* codes, int64_t N, int32_t m, int32_t b, int64_t id_base,
+                       int32_t flags, void* stream, pq_index* out) {
     PQ_API_BEGIN
     need(out != nullptr, "out is NULL");
     *out = nullptr;
@@ -351,9 +356,12 @@ pq_status pq_create(const uint8_t* codes, int64_t N, int32_t m, int32_t b, int64
                      (long long)(bad / m), (long long)(bad % m), (unsigned)v, b);
             fail(PQ_ERR_CODE_RANGE, msg);
         }
-        CreateCtx cx;
-        build_v2_layout(idx, cx, codes, src, st);
-        build_v3_layout(idx, cx, codes, src, st);
+        need((flags & ~PQ_CREATE_SMALL_BATCH_ONLY) == 0, "unknown pq_create flags");
+        if (!(flags & PQ_CREATE_SMALL_BATCH_ONLY)) {
+            CreateCtx cx;
+            build_v2_layout(idx, cx, codes, src, st);
+            build_v3_layout(idx, cx, codes, src, st);
+        }
         if (tmp) { cudaFree(tmp); tmp = nullptr; }
         cudaFree(d_bad);
         d_bad = nullptr;

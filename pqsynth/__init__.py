@@ -66,6 +66,8 @@ CONFIGS = {
                  note="graded: 50M items, item-sharded 1/2/4/8 GPUs"),
     "c6": Config("c6", 6, 10_000_000, 64, 256, 512, 256, 100,
                  note="next row f2: m = 64 splits (Fig. 2b, PAPER.md:257), not a BASELINE config"),
+    "c7": Config("c7", 7, 1_000_000_000, 8, 256, 512, 1, 10,
+                 note="next row f2: 10^9 items (RQ2, PAPER.md:255), single user; not a BASELINE config"),
     "c5": Config("c5", 5, 200_000_000, 4, 16, 64, 4096, 1000, gpus=(8,),
                  note="tie stress: 65,536 code tuples"),
 }
