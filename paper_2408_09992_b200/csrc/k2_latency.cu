@@ -157,6 +157,7 @@ __global__ void __launch_bounds__(K2L_THREADS) k2_latency(const K2LArgs a) {
                     int base = 0;
                     if (lane == 0) base = atomicAdd(&count, __popc(bm));
                     base = __shfl_sync(FULL, base, 0);
+                    if (base + __popc(bm) > CAP) __trap();     // invariant: shrink before overflow
                     if (c) cbuf[base + __popc(bm & lanemask_lt())] = keys[j];
                 }
             }

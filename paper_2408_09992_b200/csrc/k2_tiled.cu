@@ -520,6 +520,7 @@ __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
                                 if (!(cmask >> (4 * d + j) & 1u)) continue;
                                 const int u = 4 * q + j;
                                 const int p = atomicAdd(&cnt_u[u], 1);
+                                if (p >= a.cap) __trap();      // protocol invariant: cap >= wm + 2 TR
                                 ubuf[(int64_t)u * a.cap + p] = make_raw(vv[j] + 0.0f, row);
                                 if (p == wm) {
                                     *reinterpret_cast<volatile int*>(&sflag[tseq & 1]) = (int)(tseq + 1);
