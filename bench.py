@@ -195,6 +195,44 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+# ----------------------------------------------------------------------------- baselines
+def compare_paths(pq, torch, idx, cfg, F_d, P_d, S, step, flush, pq_ms, reps=3):
+    """The paper's comparison methods on the same batch, on the GPU:
+    dense scoring r = W phi (Eq. 2-3; W reconstructed once, outside the timing; fp32
+    SGEMM + top-K) and RecJPQScore (Alg. 2: split-major accumulation over an
+    N-length score array + top-K, with K1).  Speed-ups against the PQTopK step."""
+    K = cfg.K
+    W = pq.pq_reconstruct(idx, P_d)
+    torch.cuda.synchronize()
+
+    def timed(fn):
+        fn()
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(reps):
+            flush.fill_(1)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            fn()
+            e1.record()
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        return statistics.median(ts)
+
+    dws = torch.empty(max(1, int(pq.load_library().pq_dense_workspace_bytes(cfg.N, cfg.B, K))),
+                      dtype=torch.uint8, device=S.device)
+    rws = torch.empty(max(1, idx.recjpq_workspace_bytes(cfg.B, K)), dtype=torch.uint8, device=S.device)
+    dense_ms = timed(lambda: pq.pq_dense_topk(W, F_d, K, ws=dws))
+    recjpq_ms = timed(lambda: (pq.pq_subscores(F_d, P_d, S), pq.pq_recjpq_topk(idx, S, K, ws=rws)))
+    del W
+    return {"pq_ms": pq_ms, "dense_ms": dense_ms, "recjpq_ms": recjpq_ms,
+            "speedup_vs_dense": dense_ms / pq_ms, "speedup_vs_recjpq": recjpq_ms / pq_ms,
+            "dense": "W = reconstruct (Eq. 2) resident; fp32 SGEMM (no TF32) + exact top-K",
+            "recjpq": "K1 + Alg. 2 (split-major fp32 accumulator in HBM) + exact top-K",
+            "paper_cpu_context": "4.5x vs SASRec dense, 1.56x vs RecJPQ (Ryzen 5950X, TF 2.11, Gowalla "
+                                 "~1.3M items, total mRT incl. backbone; BASELINE.md)"}
+
+
 # ----------------------------------------------------------------------------- our arm
 def run_ours(args):
     import torch
@@ -405,6 +443,10 @@ def run_ours(args):
         cpu, nu, nexact = cpu_oracle_sample(cfg, codes, S.cpu().numpy(), res_ids, res_sc)
         parity = f"bit-exact vs oracle (given GPU S) on {nexact}/{nu} sampled users"
     clocks = sampler.summary()
+    comparison = None
+    want_cmp = args.compare == "on" or (args.compare == "auto" and cfg.name in ("c2", "c3"))
+    if world == 1 and want_cmp and cfg.N * d * 4 <= (48 << 30):
+        comparison = compare_paths(pq, torch, idx, cfg, F_d, P_d, S, step, flush, ms_per_step)
     line = {
         "metric": "user-item scores/s", "value": value, "unit": "user-item scores/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
@@ -425,6 +467,7 @@ def run_ours(args):
         "parity": parity,
         "clocks": clocks,
         "create_s": create_s,
+        "comparison": comparison,
         "step_ms": {"median": statistics.median(step_ms), "min": min(step_ms), "max": max(step_ms)},
     }
     print(json.dumps(line), flush=True)
@@ -441,6 +484,8 @@ def main():
     ap.add_argument("--config", default="c4", choices=sorted(pqsynth.CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--compare", default="auto", choices=["auto", "on", "off"],
+                    help="time the paper's baselines beside PQTopK (auto: c2, c3)")
     ap.add_argument("--variant", type=int, default=0, help="force K2 variant (1, 2 or 3; 0 = auto)")
     ap.add_argument("--graph", default="auto", choices=["auto", "on", "off"],
                     help="replay the step as a CUDA graph (auto: single GPU)")
