@@ -231,8 +231,11 @@ __device__ __noinline__ uint64_t shrink_user(uint64_t* ub, int nc, int n, int K,
 template <int M, int PS, int BT, int R, int W, int D>
 __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
     constexpr int NP = M / PS;
-    constexpr int NB = NP > 1 ? 2 : 1;                 // table buffers (ring; NP even -> slot = ph & 1)
-    static_assert(NP == 1 || NP % NB == 0, "ring slot must be a compile-time function of the phase");
+    // table buffers: NP == 1: one; NP > 1: a 2-slot ring (buffers 0, 1) for phases
+    // 1 .. NP-1 plus buffer 2 holding phase 0's table for the whole unit (it is
+    // the same for every tile of the unit), so a tile refills NP - 1 tables
+    constexpr int NB = NP > 1 ? 3 : 1;
+    constexpr int RES = 2;                             // resident phase-0 buffer (NP > 1)
     constexpr int LPR = R / 4;                         // lanes per row
     constexpr int RPS = 32 / LPR;                      // rows per warp slot
     constexpr int SL = 512 / W;                        // slots per warp per tile
@@ -284,10 +287,10 @@ __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
         for (uint32_t off = 0; off < TBLB; off += PIECE)
             bulk_g2s(tbl0 + buf * TBLB + off, src + off, PIECE < TBLB - off ? PIECE : TBLB - off, bar);
     };
-    // (unit, tile, phase) sequence position advanced by one
+    // ring sequence (phases 1 .. NP-1 of every tile, unit by unit) advanced by one
     auto advance = [&](int64_t& u, int64_t& t, int& ph) {
         if (++ph == NP) {
-            ph = 0;
+            ph = 1;
             if (++t == unit_tiles(u)) { t = 0; u += gridDim.x; }
         }
     };
@@ -314,13 +317,18 @@ __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
         tm_fence_after();
         tmem_base = *reinterpret_cast<volatile uint32_t*>(tmem_slot);
     }
-    // first loads: sequence positions 0 .. NB-1
+    // first loads: the unit's phase-0 table and ring positions 0, 1
     if (threadIdx.x == 0 && (int64_t)blockIdx.x < units) {
-        int64_t u = blockIdx.x, t = 0;
-        int ph = 0;
-        for (int i = 0; i < NB && u < units; ++i) {
-            issue_load(u, ph, i);
-            advance(u, t, ph);
+        if constexpr (NP == 1) {
+            issue_load(blockIdx.x, 0, 0);
+        } else {
+            issue_load(blockIdx.x, 0, RES);
+            int64_t u = blockIdx.x, t = 0;
+            int ph = 1;
+            for (int i = 0; i < 2 && u < units; ++i) {
+                issue_load(u, ph, i);
+                advance(u, t, ph);
+            }
         }
     }
 
@@ -431,8 +439,8 @@ __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
             const int64_t tile = tile0 + t;
 #pragma unroll
             for (int ph = 0; ph < NP; ++ph) {
-                const int buf = NP > 1 ? ph % NB : 0;
-                const uint32_t par = NP > 1 ? (uint32_t)((gseq / NB) & 1) : (uint32_t)(useq & 1);
+                const int buf = NP == 1 ? 0 : (ph == 0 ? RES : (int)(gseq & 1));
+                const uint32_t par = (NP == 1 || ph == 0) ? (uint32_t)(useq & 1) : (uint32_t)((gseq >> 1) & 1);
                 const int64_t tq = tseq - a.trace_from;
                 const int64_t tix = (tq >= 0 && tq % a.trace_stride == 0) ? (tq / a.trace_stride) * NP + ph : TRACE_PH;
                 const bool trc = a.trace && blockIdx.x == 0 && lane == 0 && tix < TRACE_PH;
@@ -541,13 +549,17 @@ __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
                         if (trc) a.trace[((int64_t)warp * TRACE_PH + tix) * 3 + 2] = clock64();
                         if (old == W - 1) {
                             done[buf] = 0;
-                            int64_t u2 = unit, t2 = t;
-                            int ph2 = ph;
-                            for (int st = 0; st < NB; ++st) advance(u2, t2, ph2);
-                            if (u2 < units) issue_load(u2, ph2, buf);
+                            if (ph == 0) {             // resident table: reload after the unit's last tile
+                                if (t + 1 == ntl && unit + gridDim.x < units) issue_load(unit + gridDim.x, 0, RES);
+                            } else {                   // ring: load the position this slot serves next
+                                int64_t u2 = unit, t2 = t;
+                                int ph2 = ph;
+                                for (int st = 0; st < 2; ++st) advance(u2, t2, ph2);
+                                if (u2 < units) issue_load(u2, ph2, buf);
+                            }
                         }
                     }
-                    ++gseq;
+                    if (ph > 0) ++gseq;
                 }
             }
 
@@ -701,7 +713,7 @@ int k2_tiled_rows_per_tile(int R) { return R == 32 ? 2048 : 4096; }
 
 size_t k2_tiled_smem(int m, int b, int R, int W) {
     const int ps = k2_tiled_ps(m);
-    const int nb = (m / ps) > 1 ? 2 : 1;
+    const int nb = (m / ps) > 1 ? 3 : 1;
     const size_t base = (size_t)nb * ps * b * R * 4 + (size_t)W * 1024 + (size_t)R * 8 + (size_t)R * 8 +
                         3 * 8 + 3 * 4 + (size_t)(W + 2) * 4 + 16;
     const size_t lm = nb == 1 ? (size_t)R * (32 / (R / 4)) * W * 8 : 0;   // threshold seeding keys
