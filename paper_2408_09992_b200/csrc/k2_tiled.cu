@@ -464,7 +464,7 @@ __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
 #pragma unroll 1
                 for (int s0 = 0; s0 < SL; s0 += D) {
                     float4 accs[D];                    // last phase: candidate sums of the group
-                    unsigned cmask = 0u;               // last phase: bit 4d+j = slot d, user 4q+j
+                    unsigned cmask = 0u;               // last phase: bits 4d..4d+3 = slot d's users may qualify
                     // software pipeline (single-phase tables): the gathers of slot
                     // d + 1 are issued before the adds of slot d (two slots of loads
                     // in flight); with TMEM phases the register budget favours one
@@ -512,10 +512,21 @@ __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
                         } else {
                             // last phase: branch-free candidate filter for the group
                             accs[d] = acc;
-                            cmask |= ((acc.x >= tf[0]) ? 1u : 0u) << (4 * d);
-                            cmask |= ((acc.y >= tf[1]) ? 2u : 0u) << (4 * d);
-                            cmask |= ((acc.z >= tf[2]) ? 4u : 0u) << (4 * d);
-                            cmask |= ((acc.w >= tf[3]) ? 8u : 0u) << (4 * d);
+                            if constexpr (NP == 1) {
+                                // acc + (-tf) >= 0 <=> acc >= tf exactly (IEEE subtraction keeps
+                                // the sign and is 0 only for equal operands; -inf / +inf
+                                // thresholds give +inf / -inf): a packed subtract pair and a
+                                // max tree per slot (measured faster for single-phase tables)
+                                const float2 dlo = __fadd2_rn(make_float2(acc.x, acc.y), make_float2(-tf[0], -tf[1]));
+                                const float2 dhi = __fadd2_rn(make_float2(acc.z, acc.w), make_float2(-tf[2], -tf[3]));
+                                const float mx = fmaxf(fmaxf(dlo.x, dlo.y), fmaxf(dhi.x, dhi.y));
+                                cmask |= (mx >= 0.0f ? 0xFu : 0u) << (4 * d);
+                            } else {
+                                cmask |= ((acc.x >= tf[0]) ? 1u : 0u) << (4 * d);
+                                cmask |= ((acc.y >= tf[1]) ? 2u : 0u) << (4 * d);
+                                cmask |= ((acc.z >= tf[2]) ? 4u : 0u) << (4 * d);
+                                cmask |= ((acc.w >= tf[3]) ? 8u : 0u) << (4 * d);
+                            }
                         }
                     }
                     if (ph == NP - 1 && cmask) {       // rare slow path: shared atomic + store
@@ -524,8 +535,10 @@ __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
                             const uint32_t row = row0 + (uint32_t)(s0 + d) * RPS;
                             const float vv[4] = {accs[d].x, accs[d].y, accs[d].z, accs[d].w};
 #pragma unroll
+                            if (!(cmask >> (4 * d) & 0xFu)) continue;
+#pragma unroll
                             for (int j = 0; j < 4; ++j) {
-                                if (!(cmask >> (4 * d + j) & 1u)) continue;
+                                if (!(cmask >> (4 * d + j) & 1u) || !(vv[j] >= tf[j])) continue;
                                 const int u = 4 * q + j;
                                 const int p = atomicAdd(&cnt_u[u], 1);
                                 if (p >= a.cap) __trap();      // protocol invariant: cap >= wm + 2 TR
