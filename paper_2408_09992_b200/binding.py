@@ -232,11 +232,14 @@ class PQIndex:
 
 
 SMALL_BATCH_ONLY = 1
+WITH_V2 = 2
 
 
-def pq_create(codes, b: int, id_base: int = 0, stream=None, small_batch_only: bool = False) -> PQIndex:
+def pq_create(codes, b: int, id_base: int = 0, stream=None, small_batch_only: bool = False,
+              with_v2: bool = False) -> PQIndex:
     """Build an index from codes uint8 [N][m] (numpy / CPU tensor / CUDA tensor).
-    small_batch_only: skip the batched layouts (B <= 4 serving / huge catalogues)."""
+    small_batch_only: skip the batched layouts (B <= 4 serving / huge catalogues);
+    with_v2: also build the superseded v2 kernel's layout (comparison tests)."""
     L = load_library()
     if isinstance(codes, np.ndarray):
         codes = np.ascontiguousarray(codes, dtype=np.uint8)
@@ -245,7 +248,7 @@ def pq_create(codes, b: int, id_base: int = 0, stream=None, small_batch_only: bo
     N, m = int(codes.shape[0]), int(codes.shape[1])
     h = ctypes.c_void_p()
     _check(L.pq_create_ex(ctypes.c_void_p(_ptr(codes)), N, m, int(b), int(id_base),
-                          SMALL_BATCH_ONLY if small_batch_only else 0,
+                          (SMALL_BATCH_ONLY if small_batch_only else 0) | (WITH_V2 if with_v2 else 0),
                           ctypes.c_void_p(_stream(stream)), ctypes.byref(h)))
     return PQIndex(h.value, N, m, int(b), int(id_base))
 

@@ -356,10 +356,10 @@ pq_status pq_create_ex(const uint8_t* codes, int64_t N, int32_t m, int32_t b, in
                      (long long)(bad / m), (long long)(bad % m), (unsigned)v, b);
             fail(PQ_ERR_CODE_RANGE, msg);
         }
-        need((flags & ~PQ_CREATE_SMALL_BATCH_ONLY) == 0, "unknown pq_create flags");
+        need((flags & ~(PQ_CREATE_SMALL_BATCH_ONLY | PQ_CREATE_WITH_V2)) == 0, "unknown pq_create flags");
         if (!(flags & PQ_CREATE_SMALL_BATCH_ONLY)) {
             CreateCtx cx;
-            build_v2_layout(idx, cx, codes, src, st);
+            if (flags & PQ_CREATE_WITH_V2) build_v2_layout(idx, cx, codes, src, st);
             build_v3_layout(idx, cx, codes, src, st);
         }
         if (tmp) { cudaFree(tmp); tmp = nullptr; }
@@ -415,10 +415,12 @@ pq_status pq_index_layout(pq_index idx, int32_t* paired, int32_t* tmem_splits,
                           int64_t* pairs_matched, int64_t* leftover_items) {
     PQ_API_BEGIN
     need(idx != nullptr, "index is NULL");
-    if (paired) *paired = idx->v2_ok;
-    if (tmem_splits) *tmem_splits = idx->v2_tm;
-    if (pairs_matched) *pairs_matched = idx->v2_matched;
-    if (leftover_items) *leftover_items = idx->v2_leftover;
+    // the colour pairing is shared by the v2 and v3 layouts (pq_create)
+    const bool p3 = idx->v3_ok && idx->v3_R == 16 && idx->m <= 20;
+    if (paired) *paired = (idx->v2_ok || p3) ? 1 : 0;
+    if (tmem_splits) *tmem_splits = idx->v2_ok ? idx->v2_tm : 0;
+    if (pairs_matched) *pairs_matched = idx->v2_ok ? idx->v2_matched : (p3 ? idx->v3_matched : 0);
+    if (leftover_items) *leftover_items = idx->v2_ok ? idx->v2_leftover : (p3 ? idx->v3_leftover : 0);
     PQ_API_END
 }
 

@@ -275,7 +275,7 @@ def test_paired_layout_matches_generic(pq, torch, orc, m, B, dist):
     and two v2 launch geometries agree."""
     N = 1_500_001 if m == 16 else 150_001         # m = 16: 65,536 colour classes
     G, P, F = pqsynth.random_instance(200 + m, N, m, 256, 4 * m, B, code_dist=dist)
-    idx = pq.pq_create(G, b=256, id_base=3)
+    idx = pq.pq_create(G, b=256, id_base=3, with_v2=True)
     lay = idx.layout()
     assert lay["paired"] == 1 and lay["tmem_splits"] == (2 if m == 16 else 0)
     assert idx.variants() == {1, 2, 3, 4}
