@@ -427,6 +427,10 @@ def run_ours(args):
         "per_launch": {"lookups": lookups, "algorithmic_hbm_bytes": hbm_bytes, "k2_ms": k2_avg_s * 1e3},
         "k2_share_of_step": k2_avg_s * 1e3 / ms_per_step,
         "smem_frac": achieved / peak_lookups,
+        # exact first-pair tables (b = 16): the kernel performs m - 1 lookups per pair
+        "lookups_executed_per_pair": (m - 1) if (plan["variant"] == 3 and b == 16 and m in (4, 8)) else m,
+        "smem_frac_executed": achieved / peak_lookups *
+            (((m - 1) / m) if (plan["variant"] == 3 and b == 16 and m in (4, 8)) else 1.0),
         "hbm_frac_algorithmic": (hbm_bytes / k2_avg_s) / peak_hbm,
         "peak_source_smem": f"{nsm} SMs x 32 banks x 4 B x {f_max:.0f} MHz (sm_max_mhz, {pk['source']}); "
                             "128 B/clk/SM attained by the paired LDS.128 pattern in the smem microbenchmark "

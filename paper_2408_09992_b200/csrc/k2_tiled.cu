@@ -146,7 +146,7 @@ template <int PS> struct CodePair {
     template <int RB>
     __device__ __forceinline__ uint32_t off(int e, int kk, uint32_t q16) const {
         if constexpr (K2_CODE_BYTES == 1) {
-            const uint32_t wd = w[(e * PS + kk) >> 2];
+            const uint32_t wd = w[(e * PS + kk) >> 2];     // PS here = stored codes per row
             return ((wd >> (8 * ((e * PS + kk) & 3))) & 0xFFu) * RB + q16;
         } else {
             const uint32_t wd = w[(e * PS + kk) >> 1];
@@ -227,8 +227,9 @@ __device__ __noinline__ uint64_t shrink_user(uint64_t* ub, int nc, int n, int K,
 
 // ---------------------------------------------------------------- the kernel
 // M splits, PS per phase (NP = M / PS phases), BT sub-ids, R users per table
-// row, W warps, D slots of code prefetch.
-template <int M, int PS, int BT, int R, int W, int D>
+// row, W warps, D slots of code prefetch, BT0 rows in split 0's table (BT0 !=
+// BT: the exact first-pair table, single-phase only — see below).
+template <int M, int PS, int BT, int R, int W, int D, int BT0 = BT>
 __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
     constexpr int NP = M / PS;
     // table buffers: NP == 1: one; NP > 1: a 2-slot ring (buffers 0, 1) for phases
@@ -241,10 +242,14 @@ __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
     constexpr int SL = 512 / W;                        // slots per warp per tile
     constexpr int TR = W * SL * RPS;                   // rows per tile
     constexpr uint32_t RB = R * 4;                     // bytes per table row
-    constexpr uint32_t SPLITB = (uint32_t)BT * RB;     // bytes per split table
-    constexpr uint32_t TBLB = (uint32_t)PS * SPLITB;   // bytes per table buffer
-    constexpr int CB = PS * K2_CODE_BYTES;             // code bytes per row per phase
+    constexpr uint32_t SPLITB = (uint32_t)BT * RB;     // bytes per split table (splits >= 1)
+    constexpr uint32_t TBLB = (uint32_t)(BT0 + (PS - 1) * BT) * RB;   // bytes per table buffer
+    constexpr int PSS = (PS == 3 || PS == 7) ? PS + 1 : PS;           // stored codes per row per phase
+    constexpr int CB = PSS * K2_CODE_BYTES;            // code bytes per row per phase
     static_assert(M % PS == 0, "phases");
+    static_assert(BT0 == BT || M == PS, "a first-pair table needs a single-phase table");
+    // byte offset of split kk's table inside a buffer
+    auto split_off = [](int kk) -> uint32_t { return kk == 0 ? 0u : (uint32_t)(BT0 + (kk - 1) * BT) * RB; };
     static_assert(SL % D == 0 && D % 2 == 0, "prefetch depth");
     static_assert(R == 16 || R == 32, "users per row");
 
@@ -278,7 +283,7 @@ __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
     auto issue_load = [&](int64_t u, int ph, int buf) {
         const int grp = (int)(u % a.n_groups);
         const char* src = reinterpret_cast<const char*>(a.St) +
-                          ((int64_t)grp * M + (int64_t)ph * PS) * SPLITB;
+                          (int64_t)grp * (BT0 + (M - 1) * BT) * RB + (int64_t)ph * PS * SPLITB;
         const uint32_t bar = bar0 + 8u * buf;
         fence_proxy_async();
         mbar_expect_tx(bar, TBLB);
@@ -394,7 +399,7 @@ __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
                 bool got = false;
 #pragma unroll 1
                 for (int s2 = 0; s2 < SL / 4; s2 += 2) {       // a quarter of the tile suffices
-                    CodePair<PS> cpair;
+                    CodePair<PSS> cpair;
                     cpair.load(cp + (int64_t)(s2 / 2) * 2 * RPS * CB);
 #pragma unroll
                     for (int e = 0; e < 2; ++e) {
@@ -402,7 +407,7 @@ __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
 #pragma unroll
                         for (int kk = 0; kk < PS; ++kk) {
                             const uint32_t off = cpair.template off<RB>(e, kk, q16);
-                            const float4 v = lds128(tb + kk * SPLITB + off);
+                            const float4 v = lds128(tb + split_off(kk) + off);
                             if (kk == 0) acc = v; else add4(acc, v);
                         }
                         if (a.perm[row0 + (uint32_t)(s2 + e) * RPS] >= 0) {
@@ -452,7 +457,7 @@ __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
                 // codes of this warp's slot pairs: [pair][row][2 slots][PS]
                 const char* cp = reinterpret_cast<const char*>(a.codes) + ((tile * NP + ph) * TR +
                                  ((int64_t)warp * SL * RPS + (lane / LPR) * 2)) * CB;
-                CodePair<PS> cw[DP];
+                CodePair<PSS> cw[DP];
 #pragma unroll
                 for (int d = 0; d < DP; ++d) cw[d].load(cp + d * PSTR);
                 cp += DP * PSTR;
@@ -473,7 +478,7 @@ __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
                     auto gather = [&](int d, float4 (&dst)[PS]) {
 #pragma unroll
                         for (int kk = 0; kk < PS; ++kk)
-                            dst[kk] = lds128(tb + kk * SPLITB + cw[d >> 1].template off<RB>(d & 1, kk, q16));
+                            dst[kk] = lds128(tb + split_off(kk) + cw[d >> 1].template off<RB>(d & 1, kk, q16));
                         if (d & 1) {                   // both slots of the pair addressed: refill
                             cw[d >> 1].load(cp);       // DP pairs ahead (buffer is padded)
                             cp += PSTR;
@@ -688,13 +693,46 @@ __global__ void k2_tile_S(const float* __restrict__ S, const uint8_t* __restrict
     }
 }
 
+// First-pair tables: St[g][row][w], rows 0..255 = fl(S[u][0][c % 16] + S[u][1][c / 16])
+// (the first partial sum of Eq. 5 in the sequential order), then 16 rows per
+// remaining split k = 2 .. m-1.
+__global__ void k2_tile_S_pair(const float* __restrict__ S, int B, int m, int R, int n_groups,
+                               float* __restrict__ St) {
+    const int rows = 256 + (m - 2) * 16;
+    const int64_t total = (int64_t)n_groups * rows * R;
+    for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < total;
+         x += (int64_t)gridDim.x * blockDim.x) {
+        const int w = (int)(x % R);
+        const int64_t r = x / R;
+        const int row = (int)(r % rows);
+        const int g = (int)(r / rows);
+        const int user = g * R + w;
+        float v = 0.0f;
+        if (user < B) {
+            const float* Su = S + (int64_t)user * m * 16;
+            if (row < 256) v = Su[row % 16] + Su[16 + row / 16];          // fp32 RN, split 0 then 1
+            else v = Su[(2 + (row - 256) / 16) * 16 + (row - 256) % 16];
+        }
+        St[x] = v;
+    }
+}
+
 // ---------------------------------------------------------------- host side
 typedef void (*K2TFn)(const K2TArgs);
 
-template <int M, int PS, int BT, int R>
+template <int M, int PS, int BT, int R, int BT0 = BT>
 static K2TFn tiled_fn_w(int W) {
-    if (W == 16) return k2_tiled<M, PS, BT, R, 16, 4>;
-    return k2_tiled<M, PS, BT, R, 8, 4>;
+    if (W == 16) return k2_tiled<M, PS, BT, R, 16, 4, BT0>;
+    return k2_tiled<M, PS, BT, R, 8, 4, BT0>;
+}
+// Exact first-pair tables (b = 16, m in {4, 8}): splits 0 and 1 become one
+// 256-row "split" whose row c = g0 + 16 g1 holds fl(S[0][g0] + S[1][g1]) -- the
+// first partial sum of Eq. 5 exactly as the sequential order computes it -- so
+// an item costs m - 1 lookups.
+static K2TFn tiled_pair_fn(int m_v, int W) {
+    if (m_v == 3) return tiled_fn_w<3, 3, 16, 32, 256>(W);
+    if (m_v == 7) return tiled_fn_w<7, 7, 16, 32, 256>(W);
+    return nullptr;
 }
 // Instantiated shapes: R = 16 (paired layout) for b = 256, m in {8, 16};
 // R = 32 (item order) when the 32-user table fits: (m, b) in {(4, 16), (8, 16), (4, 256)},
@@ -716,21 +754,39 @@ static K2TFn tiled_fn(int m, int b, int R, int W) {
     return nullptr;
 }
 int k2_tiled_ps(int m) { return m >= 16 ? 4 : m; }
-int k2_tiled_users(int m, int b) {
-    if (tiled_fn(m, b, 32, 16)) return 32;
-    if (tiled_fn(m, b, 16, 16)) return 16;
-    return 0;
+
+TiledShape k2_tiled_shape(int m, int b) {
+    TiledShape t{};
+    if (b == 16 && (m == 4 || m == 8) && tiled_pair_fn(m - 1, 16)) {
+        t.R = 32; t.pair = 1; t.m_v = m - 1; t.ps = m - 1; t.bt = 16; t.bt0 = 256;
+    } else if (tiled_fn(m, b, 32, 16)) {
+        t.R = 32; t.m_v = m; t.ps = k2_tiled_ps(m); t.bt = b; t.bt0 = b;
+    } else if (tiled_fn(m, b, 16, 16)) {
+        t.R = 16; t.m_v = m; t.ps = k2_tiled_ps(m); t.bt = b; t.bt0 = b;
+    } else {
+        return t;                                      // R = 0: unsupported
+    }
+    t.pss = (t.ps == 3 || t.ps == 7) ? t.ps + 1 : t.ps;
+    return t;
 }
+static K2TFn tiled_fn_shape(const TiledShape& t, int W) {
+    return t.pair ? tiled_pair_fn(t.m_v, W) : tiled_fn(t.m_v, t.bt, t.R, W);
+}
+int k2_tiled_users(int m, int b) { return k2_tiled_shape(m, b).R; }
 bool k2_tiled_supported(int m, int b) { return k2_tiled_users(m, b) > 0; }
 int k2_tiled_rows_per_tile(int R) { return R == 32 ? 2048 : 4096; }
 
-size_t k2_tiled_smem(int m, int b, int R, int W) {
-    const int ps = k2_tiled_ps(m);
-    const int nb = (m / ps) > 1 ? 3 : 1;
-    const size_t base = (size_t)nb * ps * b * R * 4 + (size_t)W * 1024 + (size_t)R * 8 + (size_t)R * 8 +
+size_t k2_tiled_smem(const TiledShape& t, int W) {
+    const int R = t.R;
+    const int nb = (t.m_v / t.ps) > 1 ? 3 : 1;
+    const size_t tbl = (size_t)(t.bt0 + (t.ps - 1) * t.bt) * R * 4;
+    const size_t base = (size_t)nb * tbl + (size_t)W * 1024 + (size_t)R * 8 + (size_t)R * 8 +
                         3 * 8 + 3 * 4 + (size_t)(W + 2) * 4 + 16;
     const size_t lm = nb == 1 ? (size_t)R * (32 / (R / 4)) * W * 8 : 0;   // threshold seeding keys
     return align_up(base, 16) + lm + 16;
+}
+static size_t st_table_bytes(const TiledShape& t, int n_groups) {
+    return (size_t)n_groups * (t.bt0 + (t.m_v - 1) * t.bt) * t.R * 4;
 }
 
 // Item chunks per user group.  Units (group x chunk) are dealt round-robin to
@@ -755,15 +811,16 @@ static int choose_chunks_tiles(int64_t n_tiles, int n_groups, int grid_full, dou
 void plan_k2_tiled(const pq_index_s* idx, int B, int K, K2Plan& p) {
     p.variant = 3;
     const pq_tuning& t = idx->tuning;
-    const int R = idx->v3_R;
+    const TiledShape sh = k2_tiled_shape(idx->m, idx->b);
+    const int R = sh.R;
     p.W = (t.warps == 8 || t.warps == 16) ? t.warps : 16;
     p.G = R; p.Ug = R; p.J = 1;
-    p.tm = (idx->m / k2_tiled_ps(idx->m)) > 1 ? idx->m - k2_tiled_ps(idx->m) : 0;
+    p.tm = (sh.m_v / sh.ps) > 1 ? sh.m_v - sh.ps : 0;
     p.n_groups = (int)ceil_div(B, R);
     const int TR = k2_tiled_rows_per_tile(R);
     p.cap = (int)align_up((size_t)(2 * K + 2 * TR + 96), 32);
-    p.smem = k2_tiled_smem(idx->m, idx->b, R, p.W);
-    K2TFn fn = tiled_fn(idx->m, idx->b, R, p.W);
+    p.smem = k2_tiled_smem(sh, p.W);
+    K2TFn fn = tiled_fn_shape(sh, p.W);
     if (!fn) fail(PQ_ERR_UNSUPPORTED, "tiled scoring kernel: unsupported shape");
     PQ_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem));
     int occ = 0;
@@ -774,7 +831,7 @@ void plan_k2_tiled(const pq_index_s* idx, int B, int K, K2Plan& p) {
     const int64_t n_tiles = idx->v3_tiles;
     p.chunks = t.chunks > 0 ? (int)std::min<int64_t>(t.chunks, n_tiles)
                             : choose_chunks_tiles(n_tiles, p.n_groups, grid_full,
-                                                  (idx->m / k2_tiled_ps(idx->m)) > 1 ? 0.3 : 0.6);
+                                                  (sh.m_v / sh.ps) > 1 ? 0.3 : 0.6);
     const int64_t ct = ceil_div(n_tiles, p.chunks);
     p.chunk_items = ct;                                // tiles per chunk
     p.chunks = (int)ceil_div(n_tiles, ct);
@@ -784,21 +841,23 @@ void plan_k2_tiled(const pq_index_s* idx, int B, int K, K2Plan& p) {
     p.cand_bytes = (size_t)B * p.chunks * K * 8;
     p.ghist_bytes = 0;
     p.mscr_bytes = 0;
-    p.st_bytes = align_up((size_t)p.n_groups * idx->m * idx->b * R * 4, 256) + (size_t)p.n_groups * R * 8;
+    p.st_bytes = align_up(st_table_bytes(sh, p.n_groups), 256) + (size_t)p.n_groups * R * 8;
 }
 
 static unsigned long long* gtau_of(const pq_index_s* idx, const K2Plan& p, const float* St) {
     return reinterpret_cast<unsigned long long*>(const_cast<char*>(reinterpret_cast<const char*>(St)) +
-                                                 align_up((size_t)p.n_groups * idx->m * idx->b * p.G * 4, 256));
+                                                 align_up(st_table_bytes(k2_tiled_shape(idx->m, idx->b), p.n_groups), 256));
 }
 
 void launch_k2_tiled_prep(const pq_index_s* idx, const K2Plan& p, const float* S, int B, float* St,
                           cudaStream_t st) {
     PQ_CUDA(cudaMemsetAsync(gtau_of(idx, p, St), 0, (size_t)p.n_groups * p.G * 8, st));
-    const int64_t total = (int64_t)p.n_groups * idx->m * idx->b * p.G;
+    const TiledShape sh = k2_tiled_shape(idx->m, idx->b);
+    const int64_t total = (int64_t)(st_table_bytes(sh, p.n_groups) / 4);
     const int threads = 256;
     const int blocks = (int)std::min<int64_t>(ceil_div(total, threads), (int64_t)idx->num_sms * 16);
-    k2_tile_S<<<blocks, threads, 0, st>>>(S, idx->d_cmap3, B, idx->m, idx->b, p.G, p.n_groups, St);
+    if (sh.pair) k2_tile_S_pair<<<blocks, threads, 0, st>>>(S, B, idx->m, p.G, p.n_groups, St);
+    else k2_tile_S<<<blocks, threads, 0, st>>>(S, idx->d_cmap3, B, idx->m, idx->b, p.G, p.n_groups, St);
     count_launch();
     check_launch("k2_tile_S");
 }
@@ -837,7 +896,7 @@ void launch_k2_tiled(const pq_index_s* idx, const K2Plan& p, int B, int K,
         PQ_CUDA(cudaMalloc(&a.trace, tn * 8));
         PQ_CUDA(cudaMemsetAsync(a.trace, 0, tn * 8, st));
     }
-    K2TFn fn = tiled_fn(idx->m, idx->b, p.G, p.W);
+    K2TFn fn = tiled_fn_shape(k2_tiled_shape(idx->m, idx->b), p.W);
     fn<<<p.grid, p.W * 32, p.smem, st>>>(a);
     count_launch();
     check_launch("k2_tiled");

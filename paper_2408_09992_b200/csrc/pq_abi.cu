@@ -206,15 +206,19 @@ static void build_v2_layout(pq_index_s* idx, CreateCtx& cx, const uint8_t* codes
 }
 
 // K2 v3 layout (k2_tiled.cu).  R = 16: the colour pairing (every split in
-// shared memory, stored codes * 64); R = 32: item order, codes * 128.  Rows are
-// padded to whole tiles and the codes phase-blocked ([tile][phase][row][PS]).
+// shared memory); R = 32: item order; with an exact first-pair table (b = 16)
+// split 0's stored code is g0 + 16 g1 and splits 2.. follow.  Rows are padded
+// to whole tiles and the codes phase-blocked ([tile][phase][row][pss], pss >=
+// ps stored bytes per row per phase).
 static void build_v3_layout(pq_index_s* idx, CreateCtx& cx, const uint8_t* codes_in, const uint8_t* dev_src,
                             cudaStream_t st) {
     const int m = idx->m, b = idx->b;
-    const int R = k2_tiled_users(m, b);
-    if (!R || k2_tiled_smem(m, b, R, 16) > idx->smem_optin) return;
+    const TiledShape sh = k2_tiled_shape(m, b);
+    const int R = sh.R;
+    if (!R || k2_tiled_smem(sh, 16) > idx->smem_optin) return;
     const int64_t N = idx->N;
     const uint8_t* hc = host_codes(cx, idx, codes_in, dev_src, st);
+    const int mv = sh.m_v;                             // stored splits per row
     PairLayout Lio;
     const PairLayout* Lp = &Lio;
     if (R == 16 && m <= 20) {
@@ -223,21 +227,25 @@ static void build_v3_layout(pq_index_s* idx, CreateCtx& cx, const uint8_t* codes
         PairLayout& L = Lio;
         L.rows = N;
         L.perm.resize((size_t)N);
-        L.codes16.resize((size_t)N * m);
+        L.codes16.resize((size_t)N * mv);
         L.cmap.resize((size_t)m * b);
         for (int k = 0; k < m; ++k)
             for (int g = 0; g < b; ++g) L.cmap[(size_t)k * b + g] = (uint8_t)g;
         for (int64_t i = 0; i < N; ++i) {
             L.perm[(size_t)i] = (int32_t)i;
-            for (int k = 0; k < m; ++k) L.codes16[(size_t)i * m + k] = (uint16_t)(hc[i * m + k] * (uint32_t)(R * 4));
+            const uint8_t* ci = hc + i * m;
+            for (int k = 0; k < mv; ++k) {
+                const uint32_t c = sh.pair ? (k == 0 ? ci[0] + 16u * ci[1] : ci[k + 1]) : ci[k];
+                L.codes16[(size_t)i * mv + k] = (uint16_t)(c * (uint32_t)(R * 4));
+            }
         }
     }
     const PairLayout& L = *Lp;
     const int64_t TR = k2_tiled_rows_per_tile(R);
     const int64_t tiles = ceil_div(L.rows, TR);
-    const int ps = k2_tiled_ps(m), np = m / ps;
+    const int ps = sh.ps, pss = sh.pss, np = mv / ps;
     const int cb = k2_tiled_code_bytes();             // 1: sub-id byte, 2: pre-shifted row offset
-    std::vector<uint8_t> c3((size_t)tiles * TR * m * cb, 0);
+    std::vector<uint8_t> c3((size_t)tiles * TR * np * pss * cb, 0);
     std::vector<int32_t> p3((size_t)tiles * TR, -1);
     // inside a phase block, slot pairs are interleaved: logical row rr = slot * RPS + r
     // is stored at ((slot / 2) * RPS + r) * 2 + slot % 2 (k2_tiled.cu, CodePair)
@@ -249,8 +257,8 @@ static void build_v3_layout(pq_index_s* idx, CreateCtx& cx, const uint8_t* codes
         p3[(size_t)r] = L.perm[(size_t)r];
         for (int ph = 0; ph < np; ++ph)
             for (int kk = 0; kk < ps; ++kk) {
-                const uint16_t v = L.codes16[(size_t)r * m + ph * ps + kk];    // stored code * R * 4
-                const size_t at = (size_t)(((t * np + ph) * TR + sr) * ps + kk);
+                const uint16_t v = L.codes16[(size_t)r * mv + ph * ps + kk];    // stored code * R * 4
+                const size_t at = (size_t)(((t * np + ph) * TR + sr) * pss + kk);
                 if (cb == 1) c3[at] = (uint8_t)(v / (uint32_t)(R * 4));
                 else reinterpret_cast<uint16_t*>(c3.data())[at] = v;
             }

@@ -138,13 +138,18 @@ void plan_k2_latency(const pq_index_s* idx, int B, int K, K2Plan& p);
 void launch_k2_latency(const pq_index_s* idx, const K2Plan& p, const float* S, int B, int K,
                        uint64_t* cand, cudaStream_t st);
 // v3 helpers (k2_tiled.cu)
+// K2 v3 kernel shape for a catalogue: R users per table row (0 = unsupported),
+// m_v "virtual" splits (m - 1 with an exact first-pair table), ps splits per
+// phase, pss stored codes per row per phase, bt / bt0 table rows (split 0: bt0)
+struct TiledShape { int R = 0, pair = 0, m_v = 0, ps = 0, pss = 0, bt = 0, bt0 = 0; };
+TiledShape k2_tiled_shape(int m, int b);
+size_t k2_tiled_smem(const TiledShape& t, int W);
 bool k2_tiled_supported(int m, int b);
 int k2_tiled_users(int m, int b);
 int k2_tiled_code_bytes();
 int k2_tiled_ps(int m);
 int k2_tiled_rows_per_tile(int R);
 constexpr int V3_CODE_PAD = 4096;     // bytes after the last tile (prefetch overhang)
-size_t k2_tiled_smem(int m, int b, int R, int W);
 void plan_k2_tiled(const pq_index_s* idx, int B, int K, K2Plan& p);
 void launch_k2_tiled_prep(const pq_index_s* idx, const K2Plan& p, const float* S, int B, float* St,
                           cudaStream_t st);
