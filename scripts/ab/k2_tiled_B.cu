@@ -722,8 +722,8 @@ typedef void (*K2TFn)(const K2TArgs);
 
 template <int M, int PS, int BT, int R, int BT0 = BT>
 static K2TFn tiled_fn_w(int W) {
-    // deeper code prefetch for m = 16 (C4: -1.7 %; m = 8 and m = 64 prefer 4)
-    if (W == 16) return k2_tiled<M, PS, BT, R, 16, (M == 16 ? 8 : 4), BT0>;
+    // deeper code prefetch for the many-split shapes (C4: -1.7 %; m = 8 prefers 4)
+    if (W == 16) return k2_tiled<M, PS, BT, R, 16, (M >= 16 ? 8 : 4), BT0>;
     return k2_tiled<M, PS, BT, R, 8, 4, BT0>;
 }
 // Exact first-pair tables (b = 16, m in {4, 8}): splits 0 and 1 become one
