@@ -266,7 +266,10 @@ def run_ours(args):
         if args.variant:
             tun["variant"] = args.variant
         idx.set_tuning(**tun)
-    plan = idx.plan(B, K)
+    # B <= 4 (the serving case): pq_search runs the whole path as ONE fused
+    # kernel (K6: sub-id scores + gather-sum + select + merge); that call is the step
+    fused = args.fused == "on" and idx.search_plan(B, d, K)["variant"] == 5
+    plan = idx.search_plan(B, d, K) if fused else idx.plan(B, K)
     layout = idx.layout()
 
     F_d = torch.from_numpy(F).to(dev)
@@ -275,6 +278,7 @@ def run_ours(args):
     ids = torch.empty((B, K), dtype=torch.int32, device=dev)
     sc = torch.empty((B, K), dtype=torch.float32, device=dev)
     ws = torch.empty(idx.topk_workspace_bytes(B, K), dtype=torch.uint8, device=dev)
+    sws = torch.empty(idx.search_workspace_bytes(B, d, K), dtype=torch.uint8, device=dev)
     if world > 1:
         out_ids = torch.empty((B, K), dtype=torch.int32, device=dev)
         out_sc = torch.empty((B, K), dtype=torch.float32, device=dev)
@@ -288,8 +292,11 @@ def run_ours(args):
         return pq.pq_merge_topk(gi, gs, ws=mws, out_ids=out_ids, out_scores=out_sc)
 
     def step():
-        pq.pq_subscores(F_d, P_d, S)
-        pq.pq_score_topk(idx, S, K, ws=ws, ids=ids, scores=sc)
+        if fused:
+            pq.pq_search(idx, F_d, P_d, K, ws=sws, ids=ids, scores=sc)
+        else:
+            pq.pq_subscores(F_d, P_d, S)
+            pq.pq_score_topk(idx, S, K, ws=ws, ids=ids, scores=sc)
         if world > 1:                                # NCCL all-gather of B x K + merge (dist.py)
             gather_merge(ids, sc, merge=merge_into_out)
 
@@ -363,7 +370,6 @@ def run_ours(args):
     P_h = torch.from_numpy(P).pin_memory()
     ids_h = torch.empty((B, K), dtype=torch.int32).pin_memory()
     sc_h = torch.empty((B, K), dtype=torch.float32).pin_memory()
-    sws = torch.empty(idx.search_workspace_bytes(B, d, K), dtype=torch.uint8, device=dev)
 
     def e2e_step():
         if world == 1:
@@ -392,7 +398,10 @@ def run_ours(args):
         dist.all_reduce(t2, op=dist.ReduceOp.MAX)
     e2e_value = B * cfg.N / (float(t2[0]) / args.steps / 1e3)
 
-    # final results for parity sampling (rank 0 at N = 1)
+    # final results for parity sampling (rank 0 at N = 1); the fused kernel's own S
+    if fused:
+        pq.pq_search(idx, F_d, P_d, K, ws=sws, ids=ids, scores=sc, S_out=S)
+    torch.cuda.synchronize()
     res_ids = (out_ids if world > 1 else ids).cpu().numpy()
     res_sc = (out_sc if world > 1 else sc).cpu().numpy()
 
@@ -417,11 +426,14 @@ def run_ours(args):
     # (m lookups per user-item pair) or, for tiny batches, the HBM stream of
     # the code matrix (m bytes per item, once per batch) -- whichever takes longer.
     hbm_bytes = n_local * m + B * m * b * 4 + B * K * 8          # algorithmic bytes per launch
+    if fused:                                        # K6 reads phi and Psi instead of S
+        hbm_bytes = n_local * m + B * d * 4 + b * d * 4 + B * K * 8
     peak_hbm = pk["hbm_gbs"] * 1e9
     t_smem, t_hbm = lookups / peak_lookups, hbm_bytes / peak_hbm
     kname = {1: "k2_score_select (v1 row groups)", 2: "k2_paired (v2)",
              3: "k2_tiled (v3: fused gather-sum-select, 4 users/lane)",
-             4: "k2_latency (v4: small-batch fused gather-sum-select)"}.get(plan["variant"], "k2")
+             4: "k2_latency (v4: small-batch fused gather-sum-select)",
+             5: "k6_query (K1 + gather-sum + select + merge in one launch, B <= 4)"}.get(plan["variant"], "k2")
     common = {
         "kernel": kname, "traffic": traffic,
         "per_launch": {"lookups": lookups, "algorithmic_hbm_bytes": hbm_bytes, "k2_ms": k2_avg_s * 1e3},
@@ -495,6 +507,8 @@ def main():
     ap.add_argument("--variant", type=int, default=0, help="force K2 variant (1, 2 or 3; 0 = auto)")
     ap.add_argument("--graph", default="auto", choices=["auto", "on", "off"],
                     help="replay the step as a CUDA graph (auto: single GPU)")
+    ap.add_argument("--fused", default="on", choices=["on", "off"],
+                    help="B <= 4: run pq_search's single-launch K6 kernel (off: K1 + K2 v4 + K3)")
     ap.add_argument("--tuning", default="", help="K2 launch tuning, e.g. warps=8,chunks=9 (diagnostics)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":

@@ -45,7 +45,7 @@
 extern "C" {
 #endif
 
-#define PQTOPK_ABI_VERSION 1
+#define PQTOPK_ABI_VERSION 2
 #define PQTOPK_MAX_K 4096        /* largest K supported by pq_score_topk & co. */
 
 typedef struct pq_index_s* pq_index;   /* opaque; immutable after pq_create */
@@ -66,14 +66,18 @@ typedef enum {
 typedef struct {
     int32_t variant;     /* 0 auto; 1 = generic row-group kernel; 2 = paired half-warps;
                             3 = tiled phases (4 users per lane, TMA tables, TMEM partials);
-                            4 = small-batch latency kernel (B <= 4, lane = item) */
+                            4 = small-batch latency kernel (B <= 4, lane = item);
+                            pq_search only: 5 = the fused single-launch query kernel (K6,
+                            B <= 4); 0 lets pq_search pick K6 whenever it applies */
     int32_t ctas;        /* persistent CTAs of the scoring kernel (0 = #SMs x occupancy) */
     int32_t warps;       /* warps per CTA of the scoring kernel (0 = auto) */
     int32_t chunks;      /* item chunks per user group (0 = auto) */
     int32_t users_per_row; /* G, table row width in users (0 = auto; power of 2, <= 32) */
     int32_t shrink_watermark; /* K2 v3 candidate-buffer shrink watermark (0 = automatic; tests
                                  use a small value to force frequent shrinks) */
-    int32_t reserved[2];
+    int32_t cluster;     /* K6: CTAs per thread-block cluster sharing one user's sub-id
+                            score computation (0 = auto (4); 1, 2, 4 or 8) */
+    int32_t reserved[1];
 } pq_tuning;
 
 /* ABI version, so a binding can refuse a mismatched library. */
@@ -144,6 +148,14 @@ pq_status pq_index_variants(pq_index idx, int32_t* mask);
  * chunks, out[6] TMEM splits, out[7] dynamic shared memory bytes.
  */
 pq_status pq_plan_info(pq_index idx, int32_t B, int32_t K, int64_t out[8]);
+
+/*
+ * The plan pq_search would use for (B, d, K): out[0] = 5 when the fused K6
+ * kernel runs (then out[1] table copies G, out[2] CTAs per cluster, out[3]
+ * warps per CTA, out[4] CTAs, out[5] item chunks per user, out[6] 0, out[7]
+ * dynamic shared memory bytes), else exactly pq_plan_info(B, K).
+ */
+pq_status pq_search_plan_info(pq_index idx, int32_t B, int32_t d, int32_t K, int64_t out[8]);
 
 /* Set launch tuning for later calls on this index (not thread-safe with
  * concurrent scoring calls on the same index). NULL restores automatic. */
@@ -221,10 +233,32 @@ size_t pq_search_workspace_bytes(pq_index idx, int32_t B, int32_t d, int32_t K);
  * through the workspace on `stream` (pinned host memory makes the copies
  * asynchronous); with host outputs the call synchronises `stream` before
  * returning.
+ *
+ * Small batches (1 <= B <= 4, m in {4, 8, 16}, K <= 512; the paper's serving
+ * case) run as ONE kernel (K6): each thread-block cluster computes one
+ * user's S (Eq. 4, the same fp64 order and single rounding as pq_subscores, so
+ * S is bit-identical), scores its item chunks (Eq. 5) and selects; the last
+ * CTA of each user merges the chunk lists (Alg. 1).  Results are
+ * bit-identical to the multi-kernel path.
  */
 pq_status pq_search(pq_index idx, const float* seq_emb, const float* subitem_emb,
                     int32_t B, int32_t d, int32_t K, void* ws, size_t ws_bytes,
                     int32_t* ids, float* scores, void* stream);
+
+/* pq_search_ex flags */
+#define PQ_SEARCH_NO_FUSED 1   /* always run K1 + K2 + K3 as separate kernels */
+
+/*
+ * pq_search_ex — pq_search with options.
+ *   flags : PQ_SEARCH_* bits (0 = as pq_search).
+ *   S_out : optional fp32 [B][m][b], DEVICE: receives the sub-id scores the
+ *           call computed (NULL = not needed).  Size the workspace with
+ *           pq_search_workspace_bytes (it covers both paths).
+ */
+pq_status pq_search_ex(pq_index idx, const float* seq_emb, const float* subitem_emb,
+                       int32_t B, int32_t d, int32_t K, int32_t flags, void* ws,
+                       size_t ws_bytes, int32_t* ids, float* scores, float* S_out,
+                       void* stream);
 
 /* Workspace bytes for pq_merge_topk. */
 size_t pq_merge_workspace_bytes(int32_t P, int32_t B, int32_t K);

@@ -26,7 +26,7 @@ MAX_K = 4096
 
 EXPORTS = ["pq_abi_version", "pq_last_error", "pq_launch_count", "pq_create", "pq_create_ex", "pq_destroy",
            "pq_index_info", "pq_index_layout", "pq_index_variants", "pq_plan_info", "pq_set_tuning", "pq_subscores", "pq_topk_workspace_bytes",
-           "pq_score_topk", "pq_search_workspace_bytes", "pq_search", "pq_merge_workspace_bytes",
+           "pq_score_topk", "pq_search_workspace_bytes", "pq_search", "pq_search_ex", "pq_search_plan_info", "pq_merge_workspace_bytes",
            "pq_merge_topk", "pq_reconstruct", "pq_dense_workspace_bytes", "pq_dense_topk",
            "pq_recjpq_workspace_bytes", "pq_recjpq_topk", "pq_timing_enable", "pq_timing_read",
            "pq_subset_workspace_bytes", "pq_score_topk_subset", "pq_exclude_workspace_bytes",
@@ -43,7 +43,8 @@ class PQError(RuntimeError):
 class Tuning(ctypes.Structure):
     _fields_ = [("variant", ctypes.c_int32), ("ctas", ctypes.c_int32), ("warps", ctypes.c_int32),
                 ("chunks", ctypes.c_int32), ("users_per_row", ctypes.c_int32),
-                ("shrink_watermark", ctypes.c_int32), ("reserved", ctypes.c_int32 * 2)]
+                ("shrink_watermark", ctypes.c_int32), ("cluster", ctypes.c_int32),
+                ("reserved", ctypes.c_int32 * 1)]
 
 
 def lib_path() -> str:
@@ -84,6 +85,8 @@ def load_library():
         "pq_score_topk_exclude": (st, [P, P, I32, I32, P, P, I32, P, SZ, P, P, P]),
         "pq_search_workspace_bytes": (SZ, [P, I32, I32, I32]),
         "pq_search": (st, [P, P, P, I32, I32, I32, P, SZ, P, P, P]),
+        "pq_search_ex": (st, [P, P, P, I32, I32, I32, I32, P, SZ, P, P, P, P]),
+        "pq_search_plan_info": (st, [P, I32, I32, I32, ctypes.POINTER(I64)]),
         "pq_merge_workspace_bytes": (SZ, [I32, I32, I32]),
         "pq_merge_topk": (st, [P, P, I32, I32, I32, P, SZ, P, P, P]),
         "pq_reconstruct": (st, [P, P, I32, P, P]),
@@ -99,7 +102,7 @@ def load_library():
         f = getattr(L, name)
         f.restype = res
         f.argtypes = args
-    if L.pq_abi_version() != 1:
+    if L.pq_abi_version() != 2:
         raise ImportError("libpqtopk ABI version mismatch")
     _lib = L
     return L
@@ -208,8 +211,21 @@ class PQIndex:
                 "tmem_splits", "smem_bytes"]
         return dict(zip(keys, [int(x) for x in out]))
 
-    def set_tuning(self, variant=0, ctas=0, warps=0, chunks=0, users_per_row=0, shrink_watermark=0):
-        t = Tuning(variant, ctas, warps, chunks, users_per_row, shrink_watermark)
+    def search_plan(self, B: int, d: int, K: int) -> dict:
+        """The plan pq_search uses for (B, d, K): variant 5 = the fused K6 kernel."""
+        out = (ctypes.c_int64 * 8)()
+        _check(load_library().pq_search_plan_info(self._h, B, d, K, out))
+        v = [int(x) for x in out]
+        if v[0] == 5:
+            keys = ["variant", "table_copies", "cluster", "warps", "ctas", "chunks", "tmem_splits", "smem_bytes"]
+        else:
+            keys = ["variant", "users_per_row", "users_per_group", "warps", "ctas", "chunks",
+                    "tmem_splits", "smem_bytes"]
+        return dict(zip(keys, v))
+
+    def set_tuning(self, variant=0, ctas=0, warps=0, chunks=0, users_per_row=0, shrink_watermark=0,
+                   cluster=0):
+        t = Tuning(variant, ctas, warps, chunks, users_per_row, shrink_watermark, cluster)
         _check(load_library().pq_set_tuning(self._h, ctypes.byref(t)))
 
     def timing_enable(self, on: bool = True):
@@ -347,10 +363,15 @@ def pq_score_topk_exclude(index: PQIndex, S, K: int, excluded, ws=None, ids=None
     return ids, scores
 
 
+SEARCH_NO_FUSED = 1
+
+
 def pq_search(index: PQIndex, seq_emb, subitem_emb, K: int, ws=None, ids=None, scores=None,
-              stream=None):
-    """The whole hot path (K1 + K2 + K3).  Inputs/outputs may be host buffers
-    (pinned CPU tensors / numpy) or CUDA tensors."""
+              stream=None, S_out=None, fused: bool = True):
+    """The whole hot path: K1 + K2 + K3, or the fused single-launch K6 kernel
+    for B <= 4 (``fused=False`` forces the multi-kernel path).  Inputs/outputs
+    may be host buffers (pinned CPU tensors / numpy) or CUDA tensors; S_out
+    (optional CUDA fp32 [B][m][b]) receives the sub-id scores."""
     torch = _torch()
     B, d = int(seq_emb.shape[0]), int(seq_emb.shape[1])
     dev = torch.device("cuda", torch.cuda.current_device())
@@ -358,13 +379,17 @@ def pq_search(index: PQIndex, seq_emb, subitem_emb, K: int, ws=None, ids=None, s
         ids = torch.empty((B, K), dtype=torch.int32, device=dev)
     if scores is None:
         scores = torch.empty((B, K), dtype=torch.float32, device=dev)
+    if S_out is not None:
+        _need_cuda(S_out, "S_out")
     L = load_library()
     nb = int(L.pq_search_workspace_bytes(index.handle, B, d, K)) if B > 0 and 0 < K <= MAX_K else 0
     ws, wsb = _ws(nb, ws, dev)
-    _check(L.pq_search(index.handle, ctypes.c_void_p(_ptr(seq_emb)), ctypes.c_void_p(_ptr(subitem_emb)),
-                       B, d, K, ctypes.c_void_p(_ptr(ws) if ws is not None else 0), wsb,
-                       ctypes.c_void_p(_ptr(ids)), ctypes.c_void_p(_ptr(scores)),
-                       ctypes.c_void_p(_stream(stream))))
+    _check(L.pq_search_ex(index.handle, ctypes.c_void_p(_ptr(seq_emb)), ctypes.c_void_p(_ptr(subitem_emb)),
+                          B, d, K, 0 if fused else SEARCH_NO_FUSED,
+                          ctypes.c_void_p(_ptr(ws) if ws is not None else 0), wsb,
+                          ctypes.c_void_p(_ptr(ids)), ctypes.c_void_p(_ptr(scores)),
+                          ctypes.c_void_p(_ptr(S_out) if S_out is not None else 0),
+                          ctypes.c_void_p(_stream(stream))))
     return ids, scores
 
 

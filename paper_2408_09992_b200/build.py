@@ -23,6 +23,8 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-ftz=false",
          "-prec-div=true", "-prec-sqrt=true", "-fmad=false", "-Xcompiler", "-Wall",
          "-I", os.path.join(HERE, "..", "include")]
+# diagnostics builds, e.g. PQTOPK_NVCC_EXTRA="-DK6_TRACE" (the K6 phase-stamp trace)
+FLAGS += os.environ.get("PQTOPK_NVCC_EXTRA", "").split()
 
 
 def _sources():

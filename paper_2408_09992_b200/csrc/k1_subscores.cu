@@ -5,7 +5,11 @@
 // Precision (R5): fp32 x fp32 products are exact in fp64, so each
 // dot product is accumulated in fp64 and rounded to fp32 once.  This meets the
 // 1e-5 relative bound per entry (plain fp32 accumulation does not, near zero)
-// and in practice reproduces fl32(exact) bit for bit.
+// and in practice reproduces fl32(exact) bit for bit.  Fixed fp64 order (R5b):
+// four partial sums c_j over t = j, j+4, j+8, ... (t < d/m, ascending), then
+// S = fl32((c_0 + c_1) + (c_2 + c_3)) -- a quarter of the dependent-add chain
+// of a sequential sum; the fused small-batch kernel (k6_query.cu) uses the same
+// order, so both produce identical S bits.
 //
 // Roofline: K1 does 2*B*b*d flops (C4: 0.27 GFLOP fp64) and writes B*m*b*4
 // bytes (C4: 16.8 MB) — a few microseconds next to K2's tens of milliseconds,
@@ -36,9 +40,9 @@ k1_subscores(const float* __restrict__ phi, const float* __restrict__ psi, int B
     const int nb = min(gchunk, b - g0);
     const int nout = nu * nb;
     constexpr int PER = (K1_UB * 256 + K1_THREADS - 1) / K1_THREADS;   // <= 16
-    double acc[PER];
+    double acc[PER][4];
 #pragma unroll
-    for (int j = 0; j < PER; ++j) acc[j] = 0.0;
+    for (int j = 0; j < PER; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.0;
 
     for (int t0 = 0; t0 < dm; t0 += K1_TT) {
         const int tt = min(K1_TT, dm - t0);
@@ -59,10 +63,18 @@ k1_subscores(const float* __restrict__ phi, const float* __restrict__ psi, int B
                 int u = o / nb, g = o - u * nb;
                 const float* pr = ps + g * (K1_TT + 1);
                 const float* fr = fs + u * K1_TT;
-                double a = acc[j];
-                for (int t = 0; t < tt; ++t)
-                    a = fma((double)pr[t], (double)fr[t], a);   // exact product, fp64 sum
-                acc[j] = a;
+                double a0 = acc[j][0], a1 = acc[j][1], a2 = acc[j][2], a3 = acc[j][3];
+                int t = 0;                              // t0 is a multiple of 4: chain = t & 3
+                for (; t + 4 <= tt; t += 4) {           // exact products, fp64 sums
+                    a0 = fma((double)pr[t], (double)fr[t], a0);
+                    a1 = fma((double)pr[t + 1], (double)fr[t + 1], a1);
+                    a2 = fma((double)pr[t + 2], (double)fr[t + 2], a2);
+                    a3 = fma((double)pr[t + 3], (double)fr[t + 3], a3);
+                }
+                if (t < tt) a0 = fma((double)pr[t], (double)fr[t], a0);
+                if (t + 1 < tt) a1 = fma((double)pr[t + 1], (double)fr[t + 1], a1);
+                if (t + 2 < tt) a2 = fma((double)pr[t + 2], (double)fr[t + 2], a2);
+                acc[j][0] = a0; acc[j][1] = a1; acc[j][2] = a2; acc[j][3] = a3;
             }
         }
     }
@@ -71,7 +83,8 @@ k1_subscores(const float* __restrict__ phi, const float* __restrict__ psi, int B
         int o = threadIdx.x + j * K1_THREADS;
         if (o < nout) {
             int u = o / nb, g = o - u * nb;
-            S[((int64_t)(u0 + u) * m + k) * b + g0 + g] = (float)acc[j];   // one rounding (RN)
+            S[((int64_t)(u0 + u) * m + k) * b + g0 + g] =
+                (float)((acc[j][0] + acc[j][1]) + (acc[j][2] + acc[j][3]));   // one rounding (RN)
         }
     }
 }

@@ -253,7 +253,8 @@ static K2Plan plan_k2_paired(const pq_index_s* idx, int B, int K) {
 }
 
 K2Plan plan_k2(const pq_index_s* idx, int B, int K) {
-    const pq_tuning& tt = idx->tuning;
+    pq_tuning tt = idx->tuning;
+    if (tt.variant == 5) tt.variant = 0;               // 5 selects K6 in pq_search only
     if (idx->v3_ok && (tt.variant == 3 || (tt.variant == 0 && tt.users_per_row == 0 && B >= 16))) {
         K2Plan p;
         plan_k2_tiled(idx, B, K, p);

@@ -405,6 +405,7 @@ pq_status pq_destroy(pq_index idx) {
         for (auto& e : *idx->events) { cudaEventDestroy(e.a); cudaEventDestroy(e.b); cudaEventDestroy(e.c); }
         delete idx->events;
     }
+    k6_cache_free(idx);
     delete idx;
     PQ_API_END
 }
@@ -458,6 +459,8 @@ pq_status pq_set_tuning(pq_index idx, const pq_tuning* t) {
         need(t->ctas >= 0 && t->chunks >= 0 && t->variant >= 0, "tuning values must be >= 0");
         need(t->users_per_row >= 0 && t->users_per_row <= 32, "tuning.users_per_row must be in [0, 32]");
         need(t->shrink_watermark >= 0, "tuning.shrink_watermark must be >= 0");
+        need(t->cluster == 0 || t->cluster == 1 || t->cluster == 2 || t->cluster == 4 || t->cluster == 8,
+             "tuning.cluster must be 0, 1, 2, 4 or 8");
         idx->tuning = *t;
     } else {
         idx->tuning = pq_tuning{};
@@ -499,6 +502,15 @@ pq_status pq_score_topk(pq_index idx, const float* S, int32_t B, int32_t K, void
     PQ_API_END
 }
 
+// pq_search runs the fused K6 kernel when it applies (B <= 4) unless the
+// caller or the tuning asks for the multi-kernel path.
+static bool use_k6(pq_index_s* idx, int B, int d, int K, int flags, K6Plan& p) {
+    if (flags & PQ_SEARCH_NO_FUSED) return false;
+    const int v = idx->tuning.variant;
+    if (v != 0 && v != 5) return false;
+    return k6_query_plan(idx, B, d, K, p);
+}
+
 size_t pq_search_workspace_bytes(pq_index idx, int32_t B, int32_t d, int32_t K) {
     try {
         if (!idx || B <= 0 || K <= 0 || K > PQTOPK_MAX_K || d < idx->m || d % idx->m) return 0;
@@ -507,7 +519,10 @@ size_t pq_search_workspace_bytes(pq_index idx, int32_t B, int32_t d, int32_t K) 
         s += align_up((size_t)B * d * 4, 256);                     // phi staging
         s += align_up((size_t)idx->b * d * 4, 256);                // psi staging
         s += 2 * align_up((size_t)B * K * 4, 256);                 // output staging
-        return s + topk_ws(idx, B, K).total;
+        size_t rest = topk_ws(idx, B, K).total;
+        K6Plan kp;
+        if (use_k6(idx, B, d, K, 0, kp)) rest = std::max(rest, k6_query_ws_bytes(kp, B));
+        return s + rest;
     } catch (const pq::Error& e) {
         set_error(e.msg);
         return 0;
@@ -517,12 +532,20 @@ size_t pq_search_workspace_bytes(pq_index idx, int32_t B, int32_t d, int32_t K) 
 pq_status pq_search(pq_index idx, const float* seq_emb, const float* subitem_emb, int32_t B,
                     int32_t d, int32_t K, void* ws, size_t ws_bytes, int32_t* ids, float* scores,
                     void* stream) {
+    return pq_search_ex(idx, seq_emb, subitem_emb, B, d, K, 0, ws, ws_bytes, ids, scores, nullptr, stream);
+}
+
+pq_status pq_search_ex(pq_index idx, const float* seq_emb, const float* subitem_emb, int32_t B,
+                       int32_t d, int32_t K, int32_t flags, void* ws, size_t ws_bytes, int32_t* ids,
+                       float* scores, float* S_out, void* stream) {
     PQ_API_BEGIN
     need(idx != nullptr, "index is NULL");
     check_topk_args(B, K);
     need(d >= idx->m && d % idx->m == 0, "d must be a positive multiple of m");
+    need((flags & ~PQ_SEARCH_NO_FUSED) == 0, "unknown pq_search_ex flags");
     if (B == 0 || K == 0) return PQ_OK;
     need(seq_emb && subitem_emb && ids && scores, "NULL pointer");
+    need(!S_out || is_device_ptr(S_out), "S_out must be device memory");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const size_t need_bytes = pq_search_workspace_bytes(idx, B, d, K);
     if (!ws || ws_bytes < need_bytes)
@@ -546,12 +569,47 @@ pq_status pq_search(pq_index idx, const float* seq_emb, const float* subitem_emb
         psi = psi_st;
     }
     const bool host_ids = !is_device_ptr(ids), host_sc = !is_device_ptr(scores);
-    launch_subscores(phi, psi, B, d, m, b, S, st);
-    run_score_topk(idx, S, B, K, rest, ws_bytes - c.off, host_ids ? ids_st : ids,
-                   host_sc ? sc_st : scores, st);
+    int32_t* ids_d = host_ids ? ids_st : ids;
+    float* sc_d = host_sc ? sc_st : scores;
+    K6Plan kp;
+    if (use_k6(idx, B, d, K, flags, kp)) {
+        pq_index_s::EvTriple ev{};
+        if (idx->timing) {
+            PQ_CUDA(cudaEventCreate(&ev.a)); PQ_CUDA(cudaEventCreate(&ev.b)); PQ_CUDA(cudaEventCreate(&ev.c));
+            PQ_CUDA(cudaEventRecord(ev.a, st));
+        }
+        launch_k6_query(idx, kp, phi, psi, B, d, K, rest, S_out, ids_d, sc_d, st);
+        if (idx->timing) {
+            PQ_CUDA(cudaEventRecord(ev.b, st));
+            PQ_CUDA(cudaEventRecord(ev.c, st));
+            idx->events->push_back(ev);
+        }
+    } else {
+        launch_subscores(phi, psi, B, d, m, b, S, st);
+        if (S_out) PQ_CUDA(cudaMemcpyAsync(S_out, S, (size_t)B * m * b * 4, cudaMemcpyDeviceToDevice, st));
+        run_score_topk(idx, S, B, K, rest, ws_bytes - c.off, ids_d, sc_d, st);
+    }
     if (host_ids) PQ_CUDA(cudaMemcpyAsync(ids, ids_st, (size_t)B * K * 4, cudaMemcpyDeviceToHost, st));
     if (host_sc) PQ_CUDA(cudaMemcpyAsync(scores, sc_st, (size_t)B * K * 4, cudaMemcpyDeviceToHost, st));
     if (host_ids || host_sc) PQ_CUDA(cudaStreamSynchronize(st));
+    PQ_API_END
+}
+
+pq_status pq_search_plan_info(pq_index idx, int32_t B, int32_t d, int32_t K, int64_t out[8]) {
+    PQ_API_BEGIN
+    need(idx != nullptr && out != nullptr, "NULL argument");
+    check_topk_args(B, K);
+    need(B > 0 && K > 0, "B and K must be > 0");
+    need(d >= idx->m && d % idx->m == 0, "d must be a positive multiple of m");
+    K6Plan kp;
+    if (use_k6(idx, B, d, K, 0, kp)) {
+        out[0] = 5; out[1] = kp.G; out[2] = kp.CL; out[3] = 8;
+        out[4] = kp.grid; out[5] = kp.chunks; out[6] = 0; out[7] = (int64_t)kp.smem;
+    } else {
+        K2Plan p = plan_k2(idx, B, K);
+        out[0] = p.variant; out[1] = p.G; out[2] = p.Ug; out[3] = p.W;
+        out[4] = p.grid; out[5] = p.chunks; out[6] = p.tm; out[7] = (int64_t)p.smem;
+    }
     PQ_API_END
 }
 

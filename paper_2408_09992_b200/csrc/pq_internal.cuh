@@ -101,6 +101,7 @@ struct pq_index_s {
     int32_t* d_perm3 = nullptr;    // [tiles * 4096] row -> local id (-1 = padding)
     uint8_t* d_cmap3 = nullptr;    // [m][b] stored -> original
     pq_tuning tuning{};
+    void* k6_cache = nullptr;      // K6 launch plans by (B, d, K, tuning) (k6_query.cu)
     // optional K2/K3 timing (pq_timing_enable)
     int timing = 0;
     struct EvTriple { cudaEvent_t a, b, c; };
@@ -132,6 +133,17 @@ struct K2Plan {
     int tm = 0;
     size_t st_bytes = 0;          // v3: tiled S tables [n_groups][m][b][16] fp32
 };
+// K6 (k6_query.cu): the fused single-launch query kernel for B <= 4
+struct K6Plan {
+    int G = 0, nst = 0, CL = 0, chunks = 0, grid = 0;
+    int64_t chunk_items = 0;
+    size_t smem = 0, cand_bytes = 0;
+};
+bool k6_query_plan(pq_index_s* idx, int B, int d, int K, K6Plan& p);   // cached per index
+void k6_cache_free(pq_index_s* idx);
+size_t k6_query_ws_bytes(const K6Plan& p, int B);
+void launch_k6_query(const pq_index_s* idx, const K6Plan& p, const float* phi, const float* psi, int B,
+                     int d, int K, void* ws, float* S_out, int32_t* ids, float* scores, cudaStream_t st);
 // v4 helpers (k2_latency.cu): small batches (B <= 4), lane = item
 bool k2_latency_supported(const pq_index_s* idx, int B, int K);
 void plan_k2_latency(const pq_index_s* idx, int B, int K, K2Plan& p);

@@ -42,7 +42,7 @@ def test_nm_exports(L):
 
 
 def test_abi_version_and_counter(L):
-    assert L.pq_abi_version() == 1
+    assert L.pq_abi_version() == 2
     assert L.pq_launch_count() >= 0
 
 

@@ -370,6 +370,76 @@ def test_latency_parity(pq, torch, orc, case):
         assert_same(i.cpu().numpy(), s.cpu().numpy(), *ref, str(tun))
 
 
+FUSED_CASES = [
+    # seed, N, m, b, d, B, K, dist — pq_search's single-launch K6 path (B <= 4)
+    (520, 10_000, 8, 256, 64, 1, 10, "uniform"),       # C1 shape
+    (521, 1_280_000, 8, 256, 512, 1, 10, "uniform"),   # C2a shape (d/m = 64)
+    (522, 70_001, 16, 256, 48, 3, 100, "uniform"),     # d/m = 3: scalar Psi loads
+    (523, 50_000, 4, 16, 64, 2, 512, "uniform"),       # heavy exact ties, K = 512
+    (524, 7, 8, 256, 32, 4, 10, "uniform"),            # K > N: padding
+    (525, 40_000, 8, 256, 40, 1, 1, "few"),            # ties, K = 1
+    (526, 300_007, 16, 200, 128, 4, 64, "zipf"),       # b not a power of 2, ragged tail
+]
+
+
+@pytest.mark.parametrize("case", FUSED_CASES, ids=[str(c[0]) for c in FUSED_CASES])
+def test_fused_query_parity(pq, torch, orc, case):
+    """K6 (K1 + K2 + K3 in one launch) is bit-exact: its S equals pq_subscores'
+    S bit for bit (and meets the 1e-5 bound vs fp64), and its ids/scores equal
+    the oracle given that S — in several cluster / chunk geometries."""
+    seed, N, m, b, d, B, K, dist = case
+    G, P, F = pqsynth.random_instance(seed, N, m, b, d, B, code_dist=dist)
+    idx = pq.pq_create(G, b=b, id_base=seed)
+    Fd, Pd = cuda(torch, F), cuda(torch, P)
+    S_ref = pq.pq_subscores(Fd, Pd).cpu().numpy()
+    check_S(orc, F, P, S_ref)
+    ref = orc.pq_topk(G, S_ref, K, id_base=seed)
+    assert idx.search_plan(B, d, K)["variant"] == 5
+    for tun in (dict(), dict(cluster=1), dict(cluster=2, chunks=6), dict(cluster=8), dict(variant=5, chunks=1)):
+        idx.set_tuning(**tun)
+        S_out = torch.full((B, m, b), float("nan"), device="cuda")
+        i, s = pq.pq_search(idx, Fd, Pd, K, S_out=S_out)
+        assert np.array_equal(S_out.cpu().numpy().view(np.uint32), S_ref.view(np.uint32)), str(tun)
+        assert_same(i.cpu().numpy(), s.cpu().numpy(), *ref, str(tun))
+    idx.set_tuning()
+    i2, s2 = pq.pq_search(idx, Fd, Pd, K, fused=False)           # the multi-kernel path agrees
+    assert_same(i2.cpu().numpy(), s2.cpu().numpy(), *ref, "fused=False")
+
+
+def test_fused_query_graph_replay_and_host_buffers(pq, torch, orc):
+    """K6's per-user completion counters are reset every call: repeated calls,
+    CUDA-graph replays and the host-buffer (e2e) path all return the same bits."""
+    G, P, F = pqsynth.random_instance(530, 200_000, 8, 256, 64, 2)
+    idx = pq.pq_create(G, b=256)
+    Fd, Pd = cuda(torch, F), cuda(torch, P)
+    S = pq.pq_subscores(Fd, Pd)
+    ref = orc.pq_topk(G, S.cpu().numpy(), 20)
+    ids = torch.empty((2, 20), dtype=torch.int32, device="cuda")
+    sc = torch.empty((2, 20), dtype=torch.float32, device="cuda")
+    ws = torch.empty(pq.load_library().pq_search_workspace_bytes(idx.handle, 2, 64, 20),
+                     dtype=torch.uint8, device="cuda")
+    for _ in range(3):
+        pq.pq_search(idx, Fd, Pd, 20, ws=ws, ids=ids, scores=sc)
+        assert_same(ids.cpu().numpy(), sc.cpu().numpy(), *ref)
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        pq.pq_search(idx, Fd, Pd, 20, ws=ws, ids=ids, scores=sc)
+    torch.cuda.current_stream().wait_stream(side)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        pq.pq_search(idx, Fd, Pd, 20, ws=ws, ids=ids, scores=sc)
+    for _ in range(3):
+        ids.fill_(-7)
+        g.replay()
+        torch.cuda.synchronize()
+        assert_same(ids.cpu().numpy(), sc.cpu().numpy(), *ref, "graph replay")
+    oi = torch.empty((2, 20), dtype=torch.int32).pin_memory()
+    os_ = torch.empty((2, 20), dtype=torch.float32).pin_memory()
+    pq.pq_search(idx, torch.from_numpy(F).pin_memory(), torch.from_numpy(P).pin_memory(), 20, ids=oi, scores=os_)
+    assert_same(oi.numpy(), os_.numpy(), *ref, "host buffers")
+
+
 SUBSET_CASES = [
     # seed, N, m, b, B, K, nV, dist
     (600, 100_000, 8, 256, 3, 10, 5_000, "uniform"),      # small batch (v4 + row map)
