@@ -285,6 +285,8 @@ def run_ours(args):
         mws_n = int(pq.load_library().pq_merge_workspace_bytes(world, B, K))
         mws = torch.empty(max(mws_n, 1), dtype=torch.uint8, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    if args.no_flush:                                # diagnostics only: the line is marked invalid
+        flush = torch.empty(0, dtype=torch.uint8, device=dev)
 
     from paper_2408_09992_b200.dist import gather_merge
 
@@ -474,7 +476,8 @@ def run_ours(args):
                    "k2_plan": plan, "layout": layout,
                    "parallelism": f"item-shard x{world}" if world > 1 else "single GPU",
                    "cuda_graph": graph is not None,
-                   "l2": "256 MiB L2 flush before every timed step (outside events)"},
+                   "l2": ("NO L2 flush (diagnostic run, not a bench value)" if args.no_flush else
+                          "256 MiB L2 flush before every timed step (outside events)")},
         "queries_per_s": B / (ms_per_step / 1e3),
         "e2e": {"value": e2e_value, "unit": "user-item scores/s",
                 "h2d_bytes_per_step": B * d * 4 + m * b * (d // m) * 4,
@@ -507,6 +510,7 @@ def main():
     ap.add_argument("--variant", type=int, default=0, help="force K2 variant (1, 2 or 3; 0 = auto)")
     ap.add_argument("--graph", default="auto", choices=["auto", "on", "off"],
                     help="replay the step as a CUDA graph (auto: single GPU)")
+    ap.add_argument("--no-flush", action="store_true", help="diagnostics: skip the L2 flush (not a valid bench line)")
     ap.add_argument("--fused", default="on", choices=["on", "off"],
                     help="B <= 4: run pq_search's single-launch K6 kernel (off: K1 + K2 v4 + K3)")
     ap.add_argument("--tuning", default="", help="K2 launch tuning, e.g. warps=8,chunks=9 (diagnostics)")

@@ -25,6 +25,7 @@
 #include <mutex>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 
 namespace cg = cooperative_groups;
 
@@ -44,7 +45,9 @@ struct K6Args {
     uint64_t* cand;            // [B][chunks][K] per-chunk lists
     uint64_t* kth;             // [B][chunks] each list's K-th key (0: fewer than K keys)
     uint64_t* kmax;            // [B][chunks] each list's largest key (0: empty)
-    unsigned int* done;        // [B] finished-chunk counters (zero at launch)
+    unsigned int* done;        // [B] finished-chunk counters, then the grid barrier (zero at launch)
+    float* Sg;                 // grid mode: [B][m][b] sub-id scores in global memory (S_out or workspace)
+    int gridsync;              // 1: cooperative grid, S computed once per user and shared through L2
     int32_t* ids;              // [B][K]
     float* scores;             // [B][K]
     int nst;                   // code stages in flight
@@ -90,9 +93,13 @@ __device__ __noinline__ void k6_block_sort(uint64_t* s, int n) { block_bitonic_d
 
 // Shared-memory bytes of the prologue region: phi_u + the cluster's S staging
 // (then reused as the candidate buffer).
-__host__ __device__ __forceinline__ size_t k6_pro_bytes(int cap_keys, int d, int E) {
+__host__ __device__ __forceinline__ size_t k6_pro_bytes(int cap_keys, int d, int E, int B) {
     const size_t pro = ((size_t)d * 8 + 15) / 16 * 16 + (size_t)E * 4;   // phi_u as fp64 | S staging
-    return ((size_t)cap_keys * 8 > pro ? (size_t)cap_keys * 8 : pro + 127) / 128 * 128;
+    const size_t prog = (size_t)B * d * 8;                                 // grid mode: phi of all users
+    size_t r = (size_t)cap_keys * 8;
+    r = pro > r ? pro : r;
+    r = prog > r ? prog : r;
+    return (r + 127) / 128 * 128;
 }
 
 // M splits, G table copies, BB = b when known at compile time (256), else 0.
@@ -111,7 +118,7 @@ __global__ void __launch_bounds__(K6_THREADS) k6_query(const K6Args a) {
     float* T = reinterpret_cast<float*>(sm_raw);                                  // [M][b][G]
     unsigned char* ring = sm_raw + tbytes;                                        // [nst][STAGE]
     unsigned char* pro = ring + (size_t)a.nst * K6_STAGE;                         // phi_u | S staging; then cbuf
-    const size_t pbytes = k6_pro_bytes(CAP, a.d, E);
+    const size_t pbytes = k6_pro_bytes(CAP, a.d, E, a.B);
     uint32_t* hist = reinterpret_cast<uint32_t*>(pro + pbytes);                   // [256]
     uint64_t* cbuf = reinterpret_cast<uint64_t*>(pro);
     double* phd = reinterpret_cast<double*>(pro);
@@ -160,7 +167,95 @@ __global__ void __launch_bounds__(K6_THREADS) k6_query(const K6Args a) {
         count = 0; tau = 0ull; seed = ~0ull; floor_key = 0ull;
     }
 
-    // ---- (1) sub-id scores of user u: this CTA's share -> every CTA's S staging
+    // ---- (1a) grid mode: the whole grid computes every user's S once (each CTA
+    // a 1/grid share of the B * m * b entries, K1's fp64 order), publishes it in
+    // global memory and meets at a grid barrier; each CTA then replicates its
+    // user's table from L2.  Co-residency is guaranteed by a cooperative launch.
+    if (a.gridsync) {
+        for (int i = threadIdx.x; i < a.B * a.d; i += K6_THREADS) phd[i] = (double)a.phi[i];
+        __syncthreads();
+        const int EB = a.B * E;
+        const int per = (EB + (int)gridDim.x - 1) / (int)gridDim.x;
+        const int e0 = (int)blockIdx.x * per, e1 = min(EB, e0 + per);
+        const int q4 = a.L / 4;
+        for (int e = e0 + (int)threadIdx.x; e < e1; e += K6_THREADS) {
+            const int uu = e / E, ee = e - uu * E;
+            const float* pr = a.psi + (int64_t)ee * a.L;
+            const double* fd = phd + (int64_t)uu * a.d + (ee / bq) * a.L;
+            double x0 = 0.0, x1 = 0.0, x2 = 0.0, x3 = 0.0;   // K1's order (R5b)
+            if ((a.L & 3) == 0 && a.L <= 64) {
+                const float4* pr4 = reinterpret_cast<const float4*>(pr);
+                float4 ra[16];
+#pragma unroll
+                for (int i = 0; i < 16; ++i)
+                    if (i < q4) ra[i] = __ldg(pr4 + i);
+#pragma unroll
+                for (int i = 0; i < 16; ++i)
+                    if (i < q4) {
+                        x0 = fma((double)ra[i].x, fd[4 * i], x0);
+                        x1 = fma((double)ra[i].y, fd[4 * i + 1], x1);
+                        x2 = fma((double)ra[i].z, fd[4 * i + 2], x2);
+                        x3 = fma((double)ra[i].w, fd[4 * i + 3], x3);
+                    }
+            } else {
+                int t = 0;
+                for (; t + 4 <= a.L; t += 4) {
+                    x0 = fma((double)__ldg(pr + t), fd[t], x0);
+                    x1 = fma((double)__ldg(pr + t + 1), fd[t + 1], x1);
+                    x2 = fma((double)__ldg(pr + t + 2), fd[t + 2], x2);
+                    x3 = fma((double)__ldg(pr + t + 3), fd[t + 3], x3);
+                }
+                if (t < a.L) x0 = fma((double)__ldg(pr + t), fd[t], x0);
+                if (t + 1 < a.L) x1 = fma((double)__ldg(pr + t + 1), fd[t + 1], x1);
+                if (t + 2 < a.L) x2 = fma((double)__ldg(pr + t + 2), fd[t + 2], x2);
+            }
+            a.Sg[e] = (float)((x0 + x1) + (x2 + x3));
+        }
+        stamp(2);
+        // grid barrier (all CTAs resident: cooperative launch)
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            unsigned int* gb = a.done + a.B;
+            __threadfence();
+            atomicAdd(gb, 1u);
+            unsigned int seen;
+            do {
+                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(gb) : "memory");
+                if (seen < gridDim.x) __nanosleep(64);
+            } while (seen < gridDim.x);
+        }
+        __syncthreads();
+        stamp(3);
+        const int rot = lane * G / 32;
+        const float* Su = a.Sg + (int64_t)u * E;
+        constexpr int RB = 16;                         // entries per thread loaded before any store
+        for (int e0r = 0; e0r < E; e0r += RB * K6_THREADS) {
+            float vv[RB];
+#pragma unroll
+            for (int q = 0; q < RB; ++q) {
+                const int e = e0r + q * K6_THREADS + (int)threadIdx.x;
+                vv[q] = e < E ? __ldcg(Su + e) : 0.0f;
+            }
+#pragma unroll
+            for (int q = 0; q < RB; ++q) {
+            const int e = e0r + q * K6_THREADS + (int)threadIdx.x;
+            if (e >= E) break;
+            const float v = vv[q];
+            if constexpr (G >= 4) {
+                constexpr int NQ = G / 4;
+                const float4 v4 = make_float4(v, v, v, v);
+                float4* dst = reinterpret_cast<float4*>(T + (size_t)e * G);
+#pragma unroll
+                for (int c = 0; c < NQ; ++c) dst[(c + rot) % NQ] = v4;
+            } else {
+#pragma unroll
+                for (int c = 0; c < G; ++c) T[(size_t)e * G + c] = v;
+            }
+            }
+        }
+        __syncthreads();
+    } else
+    // ---- (1b) cluster mode: this CTA's share of user u -> every CTA's S staging
     {
         const int per = (E + CL - 1) / CL;
         const int e0 = crank * per, e1 = min(E, e0 + per);
@@ -364,7 +459,6 @@ __global__ void __launch_bounds__(K6_THREADS) k6_query(const K6Args a) {
         }
         __syncthreads();
         if (r < 4) stamp(8 + 3 * (int)r);
-        if (threadIdx.x == 0 && r + a.nst < rounds) issue(r + a.nst);
         const int n_now = count;
         if (n_now <= K6_THREADS && n_now > a.K && (r == 0 || n_now > 2 * a.K + 32)) {
             // few candidates: rank them, keep the K best and raise the threshold to
@@ -397,6 +491,9 @@ __global__ void __launch_bounds__(K6_THREADS) k6_query(const K6Args a) {
         __syncthreads();
         if (r < 4) stamp(9 + 3 * (int)r);
         tf = tau ? key_score(tau) : -INFINITY;
+        // every thread is past this round's reads of the slot: refill it (off the
+        // barrier's critical path -- only warp 0 waits for the proxy fence)
+        if (threadIdx.x == 0 && r + a.nst < rounds) issue(r + a.nst);
         if (++slot == a.nst) { slot = 0; phase ^= 1u; }
     }
 
@@ -453,10 +550,14 @@ __global__ void __launch_bounds__(K6_THREADS) k6_query(const K6Args a) {
     uint64_t* mk = reinterpret_cast<uint64_t*>(ring) + K6_THREADS;   // ring + prologue region: merge scratch
     const uint64_t* cu = a.cand + (int64_t)u * a.chunks * a.K;
     {
+        // one pass: each thread loads its chunks' K-th and largest keys together
+        uint64_t* cm = reinterpret_cast<uint64_t*>(ring);
         uint64_t f = 0ull;
         for (int c = threadIdx.x; c < a.chunks; c += K6_THREADS) {
             const uint64_t v = __ldcg(a.kth + (int64_t)u * a.chunks + c);
+            const uint64_t mx = __ldcg(a.kmax + (int64_t)u * a.chunks + c);
             f = v > f ? v : f;
+            cm[c] = mx;
         }
 #pragma unroll
         for (int o = 16; o; o >>= 1) {
@@ -465,11 +566,8 @@ __global__ void __launch_bounds__(K6_THREADS) k6_query(const K6Args a) {
         }
         if (lane == 0) atomicMax(&floor_key, (unsigned long long)f);
         if (threadIdx.x == 0) count = 0;
+        __syncthreads();
         if (a.chunks >= a.K && a.chunks <= K6_THREADS) {
-            uint64_t* cm = reinterpret_cast<uint64_t*>(ring);
-            for (int c = threadIdx.x; c < a.chunks; c += K6_THREADS)
-                cm[c] = __ldcg(a.kmax + (int64_t)u * a.chunks + c);
-            __syncthreads();
             uint64_t mine;
             const int rk = block_rank(cm, a.chunks, mine);
             if ((int)threadIdx.x < a.chunks && rk == a.K - 1) atomicMax(&floor_key, (unsigned long long)mine);
@@ -478,15 +576,15 @@ __global__ void __launch_bounds__(K6_THREADS) k6_query(const K6Args a) {
     }
     stamp(21);
     const uint64_t fl = floor_key;
-    for (int c0 = 0; c0 < n2; c0 += 4 * K6_THREADS) {
-        uint64_t v[4];
+    for (int c0 = 0; c0 < n2; c0 += 8 * K6_THREADS) {
+        uint64_t v[8];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
+        for (int q = 0; q < 8; ++q) {
             const int i = c0 + q * K6_THREADS + threadIdx.x;
             v[q] = i < n2 ? __ldcg(cu + i) : 0ull;
         }
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
+        for (int q = 0; q < 8; ++q) {
             const bool keep = v[q] != 0ull && v[q] >= fl;
             const unsigned bm = __ballot_sync(FULL, keep);
             if (bm) {
@@ -548,7 +646,10 @@ __global__ void __launch_bounds__(K6_THREADS) k6_query(const K6Args a) {
         a.trace[(int64_t)blockIdx.x * 32 + 31] = n3;
         a.trace[(int64_t)blockIdx.x * 32 + 30] = (long long)fl;
     }
-    if (threadIdx.x == 0) a.done[u] = 0u;
+    if (threadIdx.x == 0) {
+        a.done[u] = 0u;
+        if (a.gridsync && u == 0) a.done[a.B] = 0u;   // (experiment: lets PQTOPK_K6_EXPT_NOMEMSET reuse the workspace)
+    }
     stamp(6);
 }
 
@@ -575,15 +676,16 @@ static K6Fn query_fn(int m, int G, int b) {
 }
 static int query_mp(int m) { return (m + 3) / 4 * 4; }
 static int query_cap(int m) { return 2 * (K6_STAGE / query_mp(m)); }
-static size_t query_smem(int m, int b, int G, int nst, int d) {
-    return align_up((size_t)m * b * G * 4, 128) + (size_t)nst * K6_STAGE + k6_pro_bytes(query_cap(m), d, m * b) +
+static size_t query_smem(int m, int b, int G, int nst, int d, int B) {
+    return align_up((size_t)m * b * G * 4, 128) + (size_t)nst * K6_STAGE + k6_pro_bytes(query_cap(m), d, m * b, B) +
            256 * 4;
 }
 // keys the merge scratch (ring + prologue region) holds
-static int64_t query_merge_keys(int m, int b, int nst, int d) {
-    return (int64_t)(((size_t)nst * K6_STAGE + k6_pro_bytes(query_cap(m), d, m * b)) / 8) - K6_THREADS;
+static int64_t query_merge_keys(int m, int b, int nst, int d, int B) {
+    return (int64_t)(((size_t)nst * K6_STAGE + k6_pro_bytes(query_cap(m), d, m * b, B)) / 8) - K6_THREADS;
 }
 
+// CL > 0: thread-block clusters of CL CTAs; CL == 0: cooperative grid (grid mode)
 static void query_launch_cfg(cudaLaunchConfig_t& cfg, cudaLaunchAttribute* at, int grid, size_t smem,
                              int CL, cudaStream_t st) {
     cfg = cudaLaunchConfig_t{};
@@ -591,10 +693,15 @@ static void query_launch_cfg(cudaLaunchConfig_t& cfg, cudaLaunchAttribute* at, i
     cfg.blockDim = dim3(K6_THREADS);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = (unsigned)CL;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
+    if (CL > 0) {
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = (unsigned)CL;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+    } else {
+        at[0].id = cudaLaunchAttributeCooperative;
+        at[0].val.cooperative = 1;
+    }
     cfg.attrs = at;
     cfg.numAttrs = 1;
 }
@@ -606,12 +713,13 @@ static bool plan_uncached(const pq_index_s* idx, int B, int d, int K, K6Plan& p)
     if (!query_fn(m, 1, idx->b)) return false;
     const pq_tuning& t = idx->tuning;
     int G = 16, nst = 4;
+    if (t.users_per_row > 0) G = std::min(16, pow2_ceil(t.users_per_row));   // tuning: table copies
     const size_t budget = idx->smem_optin;
-    while (G > 1 && query_smem(m, idx->b, G, 2, d) > budget) G >>= 1;
-    if (query_smem(m, idx->b, G, 2, d) > budget) return false;
-    while (nst > 2 && query_smem(m, idx->b, G, nst, d) > budget) --nst;
+    while (G > 1 && query_smem(m, idx->b, G, 2, d, B) > budget) G >>= 1;
+    if (query_smem(m, idx->b, G, 2, d, B) > budget) return false;
+    while (nst > 2 && query_smem(m, idx->b, G, nst, d, B) > budget) --nst;
     p.G = G; p.nst = nst;
-    p.smem = query_smem(m, idx->b, G, nst, d);
+    p.smem = query_smem(m, idx->b, G, nst, d, B);
     K6Fn fn = query_fn(m, G, idx->b);
     PQ_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem));
     // Cluster size CL: the CTAs of a cluster split one user's sub-id score work
@@ -623,8 +731,31 @@ static bool plan_uncached(const pq_index_s* idx, int B, int d, int K, K6Plan& p)
     // 16 KB round, measured); tuning.cluster forces one size.
     const int64_t N = idx->N;
     const int64_t ipr = K6_STAGE / query_mp(m);
-    const int64_t merge_cap = query_merge_keys(m, idx->b, nst, d);
+    const int64_t merge_cap = query_merge_keys(m, idx->b, nst, d, B);
     if (merge_cap < 2048) return false;
+    // Grid mode (default): one cooperative wave, S computed once per user by the
+    // whole grid and shared through L2 behind a grid barrier -- no per-cluster
+    // recomputation.  tuning.cluster > 0 selects the cluster mode instead.
+    if (t.cluster == 0) {
+        int per_sm = 0;
+        PQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, K6_THREADS, p.smem));
+        const int64_t cap_ctas = (int64_t)per_sm * idx->num_sms;
+        if (cap_ctas >= B) {
+            int64_t want = std::max<int64_t>(1, ceil_div(N, 512));   // >= 512 items per CTA
+            if (t.chunks > 0) want = t.chunks;
+            int64_t ch = std::max<int64_t>(1, std::min<int64_t>(want, cap_ctas / B));
+            while (ch > 1 && ch * K > merge_cap) --ch;
+            if (ch * K <= merge_cap) {
+                p.gridsync = 1;
+                p.CL = 0;
+                p.chunks = (int)ch;
+                p.chunk_items = (int64_t)align_up((size_t)ceil_div(N, ch), 16);
+                p.grid = B * (int)ch;
+                p.cand_bytes = (size_t)B * ch * K * 8;
+                return true;
+            }
+        }
+    }
     const int cands[4] = {8, 4, 2, 1};
     double best_t = 0.0;
     int CL = 0, chunks = 0;
@@ -661,7 +792,8 @@ static bool plan_uncached(const pq_index_s* idx, int B, int d, int K, K6Plan& p)
 // Plans are cached per index (the cluster-occupancy query costs host time on
 // every call otherwise); the key includes the tuning fields the plan reads.
 struct K6CacheEnt {
-    int B, d, K, chunks, cluster;
+    int B, d, K;
+    pq_tuning t;
     bool ok;
     K6Plan p;
 };
@@ -672,12 +804,12 @@ bool k6_query_plan(pq_index_s* idx, int B, int d, int K, K6Plan& p) {
     auto* v = static_cast<std::vector<K6CacheEnt>*>(idx->k6_cache);
     if (!v) idx->k6_cache = v = new std::vector<K6CacheEnt>();
     for (const auto& e : *v)
-        if (e.B == B && e.d == d && e.K == K && e.chunks == idx->tuning.chunks && e.cluster == idx->tuning.cluster) {
+        if (e.B == B && e.d == d && e.K == K && memcmp(&e.t, &idx->tuning, sizeof(pq_tuning)) == 0) {
             p = e.p;
             return e.ok;
         }
     const bool ok = plan_uncached(idx, B, d, K, p);
-    v->push_back(K6CacheEnt{B, d, K, idx->tuning.chunks, idx->tuning.cluster, ok, p});
+    v->push_back(K6CacheEnt{B, d, K, idx->tuning, ok, p});
     return ok;
 }
 
@@ -687,8 +819,9 @@ void k6_cache_free(pq_index_s* idx) {
     idx->k6_cache = nullptr;
 }
 
-size_t k6_query_ws_bytes(const K6Plan& p, int B) {
-    return align_up(p.cand_bytes, 256) + 2 * align_up((size_t)B * p.chunks * 8, 256) + align_up((size_t)B * 4, 256);
+size_t k6_query_ws_bytes(const K6Plan& p, int B, int E) {
+    return align_up(p.cand_bytes, 256) + 2 * align_up((size_t)B * p.chunks * 8, 256) +
+           align_up((size_t)(B + 1) * 4, 256) + align_up((size_t)B * E * 4, 256);
 }
 
 void launch_k6_query(const pq_index_s* idx, const K6Plan& p, const float* phi, const float* psi, int B,
@@ -707,9 +840,14 @@ void launch_k6_query(const pq_index_s* idx, const K6Plan& p, const float* phi, c
     a.kth = reinterpret_cast<uint64_t*>(w + align_up(p.cand_bytes, 256));
     a.kmax = reinterpret_cast<uint64_t*>(w + align_up(p.cand_bytes, 256) + kb);
     a.done = reinterpret_cast<unsigned int*>(w + align_up(p.cand_bytes, 256) + 2 * kb);
+    a.Sg = S_out ? S_out
+                 : reinterpret_cast<float*>(w + align_up(p.cand_bytes, 256) + 2 * kb + align_up((size_t)(B + 1) * 4, 256));
+    a.gridsync = p.gridsync;
+    if (p.gridsync) a.S_out = nullptr;              // written through Sg
     a.ids = ids; a.scores = scores;
     a.nst = p.nst;
-    PQ_CUDA(cudaMemsetAsync(a.done, 0, (size_t)B * 4, st));
+    static const bool no_memset = getenv("PQTOPK_K6_EXPT_NOMEMSET") != nullptr;   // experiment only
+    if (!no_memset) PQ_CUDA(cudaMemsetAsync(a.done, 0, (size_t)(B + 1) * 4, st));
     cudaLaunchConfig_t cfg;
     cudaLaunchAttribute at[1];
     query_launch_cfg(cfg, at, p.grid, p.smem, p.CL, st);

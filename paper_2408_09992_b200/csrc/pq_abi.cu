@@ -521,7 +521,7 @@ size_t pq_search_workspace_bytes(pq_index idx, int32_t B, int32_t d, int32_t K) 
         s += 2 * align_up((size_t)B * K * 4, 256);                 // output staging
         size_t rest = topk_ws(idx, B, K).total;
         K6Plan kp;
-        if (use_k6(idx, B, d, K, 0, kp)) rest = std::max(rest, k6_query_ws_bytes(kp, B));
+        if (use_k6(idx, B, d, K, 0, kp)) rest = std::max(rest, k6_query_ws_bytes(kp, B, idx->m * idx->b));
         return s + rest;
     } catch (const pq::Error& e) {
         set_error(e.msg);
@@ -603,7 +603,7 @@ pq_status pq_search_plan_info(pq_index idx, int32_t B, int32_t d, int32_t K, int
     need(d >= idx->m && d % idx->m == 0, "d must be a positive multiple of m");
     K6Plan kp;
     if (use_k6(idx, B, d, K, 0, kp)) {
-        out[0] = 5; out[1] = kp.G; out[2] = kp.CL; out[3] = 8;
+        out[0] = 5; out[1] = kp.G; out[2] = kp.gridsync ? 0 : kp.CL; out[3] = 8;
         out[4] = kp.grid; out[5] = kp.chunks; out[6] = 0; out[7] = (int64_t)kp.smem;
     } else {
         K2Plan p = plan_k2(idx, B, K);
