@@ -172,23 +172,29 @@ __global__ void __launch_bounds__(K6_THREADS) k6_query(const K6Args a) {
     // global memory and meets at a grid barrier; each CTA then replicates its
     // user's table from L2.  Co-residency is guaranteed by a cooperative launch.
     if (a.gridsync) {
-        for (int i = threadIdx.x; i < a.B * a.d; i += K6_THREADS) phd[i] = (double)a.phi[i];
-        __syncthreads();
         const int EB = a.B * E;
         const int per = (EB + (int)gridDim.x - 1) / (int)gridDim.x;
         const int e0 = (int)blockIdx.x * per, e1 = min(EB, e0 + per);
         const int q4 = a.L / 4;
-        for (int e = e0 + (int)threadIdx.x; e < e1; e += K6_THREADS) {
-            const int uu = e / E, ee = e - uu * E;
-            const float* pr = a.psi + (int64_t)ee * a.L;
-            const double* fd = phd + (int64_t)uu * a.d + (ee / bq) * a.L;
-            double x0 = 0.0, x1 = 0.0, x2 = 0.0, x3 = 0.0;   // K1's order (R5b)
-            if ((a.L & 3) == 0 && a.L <= 64) {
-                const float4* pr4 = reinterpret_cast<const float4*>(pr);
-                float4 ra[16];
+        // the usual case, at most one entry per thread: its Psi row is requested
+        // before phi is staged, so the two memory latencies overlap
+        const bool one = per <= K6_THREADS && (a.L & 3) == 0 && a.L <= 64;
+        const int em = e0 + (int)threadIdx.x;
+        const bool has = one && em < e1;
+        float4 ra[16];
+        if (has) {
+            const float4* pr4 = reinterpret_cast<const float4*>(a.psi + (int64_t)(em % E) * a.L);
 #pragma unroll
-                for (int i = 0; i < 16; ++i)
-                    if (i < q4) ra[i] = __ldg(pr4 + i);
+            for (int i = 0; i < 16; ++i)
+                if (i < q4) ra[i] = __ldg(pr4 + i);
+        }
+        for (int i = threadIdx.x; i < a.B * a.d; i += K6_THREADS) phd[i] = (double)a.phi[i];
+        __syncthreads();
+        if (one) {
+            if (has) {
+                const int uu = em / E, ee = em - uu * E;
+                const double* fd = phd + (int64_t)uu * a.d + (ee / bq) * a.L;
+                double x0 = 0.0, x1 = 0.0, x2 = 0.0, x3 = 0.0;   // K1's order (R5b)
 #pragma unroll
                 for (int i = 0; i < 16; ++i)
                     if (i < q4) {
@@ -197,24 +203,33 @@ __global__ void __launch_bounds__(K6_THREADS) k6_query(const K6Args a) {
                         x2 = fma((double)ra[i].z, fd[4 * i + 2], x2);
                         x3 = fma((double)ra[i].w, fd[4 * i + 3], x3);
                     }
-            } else {
-                int t = 0;
-                for (; t + 4 <= a.L; t += 4) {
-                    x0 = fma((double)__ldg(pr + t), fd[t], x0);
-                    x1 = fma((double)__ldg(pr + t + 1), fd[t + 1], x1);
-                    x2 = fma((double)__ldg(pr + t + 2), fd[t + 2], x2);
-                    x3 = fma((double)__ldg(pr + t + 3), fd[t + 3], x3);
-                }
-                if (t < a.L) x0 = fma((double)__ldg(pr + t), fd[t], x0);
-                if (t + 1 < a.L) x1 = fma((double)__ldg(pr + t + 1), fd[t + 1], x1);
-                if (t + 2 < a.L) x2 = fma((double)__ldg(pr + t + 2), fd[t + 2], x2);
+                a.Sg[em] = (float)((x0 + x1) + (x2 + x3));
             }
+        } else
+        for (int e = e0 + (int)threadIdx.x; e < e1; e += K6_THREADS) {
+            const int uu = e / E, ee = e - uu * E;
+            const float* pr = a.psi + (int64_t)ee * a.L;
+            const double* fd = phd + (int64_t)uu * a.d + (ee / bq) * a.L;
+            double x0 = 0.0, x1 = 0.0, x2 = 0.0, x3 = 0.0;   // K1's order (R5b)
+            int t = 0;
+            for (; t + 4 <= a.L; t += 4) {
+                x0 = fma((double)__ldg(pr + t), fd[t], x0);
+                x1 = fma((double)__ldg(pr + t + 1), fd[t + 1], x1);
+                x2 = fma((double)__ldg(pr + t + 2), fd[t + 2], x2);
+                x3 = fma((double)__ldg(pr + t + 3), fd[t + 3], x3);
+            }
+            if (t < a.L) x0 = fma((double)__ldg(pr + t), fd[t], x0);
+            if (t + 1 < a.L) x1 = fma((double)__ldg(pr + t + 1), fd[t + 1], x1);
+            if (t + 2 < a.L) x2 = fma((double)__ldg(pr + t + 2), fd[t + 2], x2);
             a.Sg[e] = (float)((x0 + x1) + (x2 + x3));
         }
         stamp(2);
         // grid barrier (all CTAs resident: cooperative launch)
         __syncthreads();
         if (threadIdx.x == 0) {
+            // the counters are zeroed by the preceding k6_reset launch (programmatic
+            // dependent launch: everything above overlapped it)
+            asm volatile("griddepcontrol.wait;" ::: "memory");
             unsigned int* gb = a.done + a.B;
             __threadfence();
             atomicAdd(gb, 1u);
@@ -537,7 +552,10 @@ __global__ void __launch_bounds__(K6_THREADS) k6_query(const K6Args a) {
     __threadfence();                                   // publish this chunk's list (device scope)
     __syncthreads();
     stamp(5);
-    if (threadIdx.x == 0) is_last = atomicAdd(&a.done[u], 1u) == (unsigned)(a.chunks - 1);
+    if (threadIdx.x == 0) {
+        asm volatile("griddepcontrol.wait;" ::: "memory");   // (no-op once waited)
+        is_last = atomicAdd(&a.done[u], 1u) == (unsigned)(a.chunks - 1);
+    }
     __syncthreads();
     if (!is_last) return;
 
@@ -646,11 +664,16 @@ __global__ void __launch_bounds__(K6_THREADS) k6_query(const K6Args a) {
         a.trace[(int64_t)blockIdx.x * 32 + 31] = n3;
         a.trace[(int64_t)blockIdx.x * 32 + 30] = (long long)fl;
     }
-    if (threadIdx.x == 0) {
-        a.done[u] = 0u;
-        if (a.gridsync && u == 0) a.done[a.B] = 0u;   // (experiment: lets PQTOPK_K6_EXPT_NOMEMSET reuse the workspace)
-    }
+    if (threadIdx.x == 0) a.done[u] = 0u;
     stamp(6);
+}
+
+// Zeroes the call's completion counters; lets the K6 launch that follows start
+// at once (programmatic dependent launch) -- K6 waits (griddepcontrol.wait)
+// only before its first counter access, after its prologue.
+__global__ void k6_reset(unsigned int* c, int n) {
+    asm volatile("griddepcontrol.launch_dependents;");
+    for (int i = threadIdx.x; i < n; i += blockDim.x) c[i] = 0u;
 }
 
 // ---------------------------------------------------------------- host side
@@ -687,7 +710,7 @@ static int64_t query_merge_keys(int m, int b, int nst, int d, int B) {
 
 // CL > 0: thread-block clusters of CL CTAs; CL == 0: cooperative grid (grid mode)
 static void query_launch_cfg(cudaLaunchConfig_t& cfg, cudaLaunchAttribute* at, int grid, size_t smem,
-                             int CL, cudaStream_t st) {
+                             int CL, cudaStream_t st, bool pdl = false) {
     cfg = cudaLaunchConfig_t{};
     cfg.gridDim = dim3((unsigned)grid);
     cfg.blockDim = dim3(K6_THREADS);
@@ -704,6 +727,11 @@ static void query_launch_cfg(cudaLaunchConfig_t& cfg, cudaLaunchAttribute* at, i
     }
     cfg.attrs = at;
     cfg.numAttrs = 1;
+    if (pdl) {
+        at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[1].val.programmaticStreamSerializationAllowed = 1;
+        cfg.numAttrs = 2;
+    }
 }
 
 static bool plan_uncached(const pq_index_s* idx, int B, int d, int K, K6Plan& p) {
@@ -846,11 +874,17 @@ void launch_k6_query(const pq_index_s* idx, const K6Plan& p, const float* phi, c
     if (p.gridsync) a.S_out = nullptr;              // written through Sg
     a.ids = ids; a.scores = scores;
     a.nst = p.nst;
-    static const bool no_memset = getenv("PQTOPK_K6_EXPT_NOMEMSET") != nullptr;   // experiment only
-    if (!no_memset) PQ_CUDA(cudaMemsetAsync(a.done, 0, (size_t)(B + 1) * 4, st));
+    static const bool no_pdl = getenv("PQTOPK_K6_NO_PDL") != nullptr;   // diagnostics: plain memset + launch
+    if (no_pdl) {
+        PQ_CUDA(cudaMemsetAsync(a.done, 0, (size_t)(B + 1) * 4, st));
+    } else {
+        k6_reset<<<1, 32, 0, st>>>(a.done, B + 1);
+        count_launch();
+        check_launch("k6_reset");
+    }
     cudaLaunchConfig_t cfg;
-    cudaLaunchAttribute at[1];
-    query_launch_cfg(cfg, at, p.grid, p.smem, p.CL, st);
+    cudaLaunchAttribute at[2];
+    query_launch_cfg(cfg, at, p.grid, p.smem, p.CL, st, !no_pdl);
     const char* tf = getenv("PQTOPK_K6_TRACE");
     if (tf && *tf) {
         PQ_CUDA(cudaMalloc(&a.trace, (size_t)p.grid * 32 * 8));
