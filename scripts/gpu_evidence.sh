@@ -18,3 +18,8 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --c
 for c in ${PROFCFG:-c4 c5}; do
 timeout 1200 ncu --set full --clock-control none --import-source on -k regex:k2_tiled -s 3 -c 1 -o gpurun_out/k2_${c}_${TAG} python bench.py --config $c --steps 1 --warmup 3 --no-cpu-baseline --graph off > gpurun_out/ncu_full_${c}_${TAG}.log 2>&1; echo ncu_full_$c=$?
 done
+# the fused small-batch kernel (K6): launch list and one full capture on the B = 1 configs
+for c in ${K6CFG:-c2a c1}; do
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv --log-file gpurun_out/launches_${c}_${TAG}.csv python bench.py --config $c --steps 2 --warmup 3 --no-cpu-baseline --graph off > /dev/null 2>&1; echo ncu_launch_$c=$?
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k6_query -s 3 -c 1 -o gpurun_out/k6_${c}_${TAG} python bench.py --config $c --steps 1 --warmup 3 --no-cpu-baseline --graph off > gpurun_out/ncu_full_k6_${c}_${TAG}.log 2>&1; echo ncu_full_k6_$c=$?
+done
