@@ -210,6 +210,13 @@ static void build_v2_layout(pq_index_s* idx, CreateCtx& cx, const uint8_t* codes
 // split 0's stored code is g0 + 16 g1 and splits 2.. follow.  Rows are padded
 // to whole tiles and the codes phase-blocked ([tile][phase][row][pss], pss >=
 // ps stored bytes per row per phase).
+static void free_index_buffers(pq_index_s* idx) {
+    void* bufs[] = {idx->d_codes, idx->d_perm, idx->d_cmap, idx->d_codes16, idx->d_perm16, idx->d_cmap16,
+                    idx->d_pos16, idx->d_codes3, idx->d_perm3, idx->d_cmap3};
+    for (void* p : bufs)
+        if (p) cudaFree(p);
+}
+
 static void build_v3_layout(pq_index_s* idx, CreateCtx& cx, const uint8_t* codes_in, const uint8_t* dev_src,
                             cudaStream_t st) {
     const int m = idx->m, b = idx->b;
@@ -376,12 +383,7 @@ pq_status pq_create_ex(const uint8_t* codes, int64_t N, int32_t m, int32_t b, in
     } catch (...) {
         if (tmp) cudaFree(tmp);
         if (d_bad) cudaFree(d_bad);
-        if (idx->d_codes) cudaFree(idx->d_codes);
-        if (idx->d_codes16) cudaFree(idx->d_codes16);
-        if (idx->d_perm16) cudaFree(idx->d_perm16);
-        if (idx->d_cmap16) cudaFree(idx->d_cmap16);
-        if (idx->d_pos16) cudaFree(idx->d_pos16);
-        if (idx->d_codes3) cudaFree(idx->d_codes3);
+        free_index_buffers(idx);
         delete idx;
         throw;
     }
@@ -393,14 +395,7 @@ pq_status pq_destroy(pq_index idx) {
     PQ_API_BEGIN
     if (!idx) return PQ_OK;
     cudaDeviceSynchronize();
-    if (idx->d_codes) cudaFree(idx->d_codes);
-    if (idx->d_perm) cudaFree(idx->d_perm);
-    if (idx->d_cmap) cudaFree(idx->d_cmap);
-    if (idx->d_codes16) cudaFree(idx->d_codes16);
-    if (idx->d_perm16) cudaFree(idx->d_perm16);
-    if (idx->d_cmap16) cudaFree(idx->d_cmap16);
-    if (idx->d_pos16) cudaFree(idx->d_pos16);
-    if (idx->d_codes3) cudaFree(idx->d_codes3);
+    free_index_buffers(idx);
     if (idx->events) {
         for (auto& e : *idx->events) { cudaEventDestroy(e.a); cudaEventDestroy(e.b); cudaEventDestroy(e.c); }
         delete idx->events;

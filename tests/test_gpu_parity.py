@@ -488,3 +488,25 @@ def test_exclude_parity(pq, torch, orc, B, K, dist):
         ri, rs = orc.pq_topk(G[keep], S_h[u:u + 1], K)
         ri = np.where(ri >= 0, keep[np.clip(ri, 0, None)] + 11, -1).astype(np.int32)
         assert_same(ids.cpu().numpy()[u:u + 1], sc.cpu().numpy()[u:u + 1], ri, rs, str(u))
+
+
+def test_create_destroy_frees_device_memory(pq, torch):
+    """pq_destroy (and a failed pq_create) release every device buffer of the
+    index, including the tiled (v3) layout's row map and colour map."""
+    G, P, F = pqsynth.random_instance(700, 1_000_000, 8, 256, 64, 1)
+    idx = pq.pq_create(G, b=256)                       # warm-up: allocator / context state
+    idx.close()
+    torch.cuda.synchronize()
+    free0 = torch.cuda.mem_get_info()[0]
+    for _ in range(4):
+        idx = pq.pq_create(G, b=256)
+        assert idx.layout()["paired"] == 1
+        idx.close()
+    bad = G.copy()
+    bad[123, 3] = 255
+    for _ in range(2):
+        with pytest.raises(pq.PQError):
+            pq.pq_create(bad, b=200)                   # code out of range: nothing may leak
+    torch.cuda.synchronize()
+    free1 = torch.cuda.mem_get_info()[0]
+    assert free0 - free1 < (8 << 20), (free0, free1)
