@@ -86,6 +86,13 @@ struct K2TArgs {
     int trace_from;            // first traced tile of CTA 0 (PQTOPK_K2_TRACE_FROM)
     int* dbg;                  // diagnostics (PQTOPK_K2_DEBUG): bounded spins record state here
 };
+// Phase traces are compiled in only for diagnostics builds (PQTOPK_NVCC_EXTRA=-DK2_TRACE);
+// otherwise every trace branch folds away.
+#ifdef K2_TRACE
+constexpr bool kTrace = true;
+#else
+constexpr bool kTrace = false;
+#endif
 constexpr int TRACE_PH = 256;  // traced table uses (CTA 0): [W][TRACE_PH][3]; then CTA 0 units [TRACE_PH/2][2];
 constexpr int TRACE_CTAS = 1024;  // then per-CTA [TRACE_CTAS][3] = (start ns, end ns, tiles)
 
@@ -358,11 +365,11 @@ __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
     constexpr int64_t PSTR = 2 * RPS * CB;             // code bytes per slot pair
     constexpr int DP = D / 2;                          // slot pairs per group
     __shared__ unsigned long long t_start_ns;
-    if (a.trace && threadIdx.x == 0) {
+    if (kTrace && a.trace && threadIdx.x == 0) {
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start_ns));
     }
     for (int64_t unit = blockIdx.x; unit < units; unit += gridDim.x) {
-        if (a.trace && blockIdx.x == 0 && threadIdx.x == 0 && useq < TRACE_PH / 2)
+        if (kTrace && a.trace && blockIdx.x == 0 && threadIdx.x == 0 && useq < TRACE_PH / 2)
             a.trace[(int64_t)W * TRACE_PH * 3 + 2 * useq] = clock64();
         const int chunk = (int)(unit / a.n_groups);
         const int grp = (int)(unit - (int64_t)chunk * a.n_groups);
@@ -444,9 +451,13 @@ __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
             for (int ph = 0; ph < NP; ++ph) {
                 const int buf = NP == 1 ? 0 : (ph == 0 ? RES : (int)(gseq & 1));
                 const uint32_t par = (NP == 1 || ph == 0) ? (uint32_t)(useq & 1) : (uint32_t)((gseq >> 1) & 1);
-                const int64_t tq = tseq - a.trace_from;
-                const int64_t tix = (tq >= 0 && tq % a.trace_stride == 0) ? (tq / a.trace_stride) * NP + ph : TRACE_PH;
-                const bool trc = a.trace && blockIdx.x == 0 && lane == 0 && tix < TRACE_PH;
+                int64_t tix = TRACE_PH;
+                bool trc = false;
+                if constexpr (kTrace) {
+                    const int64_t tq = tseq - a.trace_from;
+                    tix = (tq >= 0 && tq % a.trace_stride == 0) ? (tq / a.trace_stride) * NP + ph : TRACE_PH;
+                    trc = a.trace && blockIdx.x == 0 && lane == 0 && tix < TRACE_PH;
+                }
                 if (trc) a.trace[((int64_t)warp * TRACE_PH + tix) * 3 + 0] = clock64();
                 mbar_wait(bar0 + 8u * buf, par);
                 if (trc) a.trace[((int64_t)warp * TRACE_PH + tix) * 3 + 1] = clock64();
@@ -652,11 +663,11 @@ __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
         }
         __syncthreads();
         if (threadIdx.x < R) { tau_sh[threadIdx.x] = 0ull; cnt_u[threadIdx.x] = 0; nconv_u[threadIdx.x] = 0; }
-        if (a.trace && blockIdx.x == 0 && threadIdx.x == 0 && useq < TRACE_PH / 2)
+        if (kTrace && a.trace && blockIdx.x == 0 && threadIdx.x == 0 && useq < TRACE_PH / 2)
             a.trace[(int64_t)W * TRACE_PH * 3 + 2 * useq + 1] = clock64();
         ++useq;
     }
-    if (a.trace && threadIdx.x == 0 && blockIdx.x < TRACE_CTAS) {
+    if (kTrace && a.trace && threadIdx.x == 0 && blockIdx.x < TRACE_CTAS) {
         unsigned long long t_end_ns;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end_ns));
         long long* c = a.trace + (int64_t)W * TRACE_PH * 3 + TRACE_PH + 3 * blockIdx.x;
@@ -893,6 +904,7 @@ void launch_k2_tiled(const pq_index_s* idx, const K2Plan& p, int B, int K,
     a.trace_from = tfr ? std::max(0, atoi(tfr)) : 0;
     const size_t tn = (size_t)p.W * TRACE_PH * 3 + TRACE_PH + 3 * TRACE_CTAS;
     if (tf && *tf) {
+        if (!kTrace) fprintf(stderr, "PQTOPK_K2_TRACE: rebuild with PQTOPK_NVCC_EXTRA=-DK2_TRACE to record traces\n");
         PQ_CUDA(cudaMalloc(&a.trace, tn * 8));
         PQ_CUDA(cudaMemsetAsync(a.trace, 0, tn * 8, st));
     }
