@@ -281,14 +281,15 @@ __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
     const uint32_t bar0 = smem_u32(mbar);
 
     const int64_t units = (int64_t)a.n_groups * a.chunks;
+    // units < 2^31 (user groups x chunks): 32-bit unsigned division, no 64-bit call
     auto unit_tiles = [&](int64_t u) -> int64_t {
-        const int64_t ch = u / a.n_groups;
+        const int64_t ch = (int64_t)((uint32_t)u / (uint32_t)a.n_groups);
         const int64_t t0 = ch * a.chunk_tiles;
         return min(a.n_tiles, t0 + a.chunk_tiles) - t0;
     };
     // TMA bulk copy: tables of (unit, phase) -> ring buffer `buf`
     auto issue_load = [&](int64_t u, int ph, int buf) {
-        const int grp = (int)(u % a.n_groups);
+        const int grp = (int)((uint32_t)u % (uint32_t)a.n_groups);
         const char* src = reinterpret_cast<const char*>(a.St) +
                           (int64_t)grp * (BT0 + (M - 1) * BT) * RB + (int64_t)ph * PS * SPLITB;
         const uint32_t bar = bar0 + 8u * buf;
@@ -371,7 +372,7 @@ __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
     for (int64_t unit = blockIdx.x; unit < units; unit += gridDim.x) {
         if (kTrace && a.trace && blockIdx.x == 0 && threadIdx.x == 0 && useq < TRACE_PH / 2)
             a.trace[(int64_t)W * TRACE_PH * 3 + 2 * useq] = clock64();
-        const int chunk = (int)(unit / a.n_groups);
+        const int chunk = (int)((uint32_t)unit / (uint32_t)a.n_groups);
         const int grp = (int)(unit - (int64_t)chunk * a.n_groups);
         const int64_t tile0 = (int64_t)chunk * a.chunk_tiles;
         const int64_t ntl = unit_tiles(unit);
@@ -847,6 +848,7 @@ void plan_k2_tiled(const pq_index_s* idx, int B, int K, K2Plan& p) {
     p.chunk_items = ct;                                // tiles per chunk
     p.chunks = (int)ceil_div(n_tiles, ct);
     const int64_t units = (int64_t)p.n_groups * p.chunks;
+    if (units >= ((int64_t)1 << 31)) fail(PQ_ERR_UNSUPPORTED, "tiled scoring kernel: too many work units");
     p.grid = (int)std::min<int64_t>(units, t.ctas > 0 ? t.ctas : grid_full);
     p.lanebuf_bytes = (size_t)p.grid * R * p.cap * 8;
     p.cand_bytes = (size_t)B * p.chunks * K * 8;

@@ -1,4 +1,5 @@
-"""Read a PQTOPK_K2_TRACE dump (CTA 0 phase timeline of k2_tiled) and print skew / wait stats."""
+"""Read a PQTOPK_K2_TRACE dump (CTA 0 phase timeline of k2_tiled) and print skew / wait stats.
+The library must be built with PQTOPK_NVCC_EXTRA=-DK2_TRACE (python -m paper_2408_09992_b200.build --force)."""
 import sys
 import numpy as np
 raw = open(sys.argv[1], "rb").read()
