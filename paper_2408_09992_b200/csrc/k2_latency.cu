@@ -77,7 +77,7 @@ __global__ void __launch_bounds__(K2L_THREADS) k2_latency(const K2LArgs a) {
         // position g0 + r (slot (g0 + r) % nst), g0 = rounds consumed before the unit
         const int64_t g0 = g;
         auto issue = [&](int64_t r) {
-            const int slot = (int)((g0 + r) % a.nst);
+            const int slot = (int)((uint32_t)(g0 + r) % (uint32_t)a.nst);   // rounds per CTA < 2^32
             const int64_t s0 = i0 + r * IPR;
             const uint32_t bytes = (uint32_t)align_up((size_t)(min((int64_t)IPR, i1 - s0) * MP), 16);
             const uint32_t bar = bar0 + 8u * slot;
@@ -119,8 +119,9 @@ __global__ void __launch_bounds__(K2L_THREADS) k2_latency(const K2LArgs a) {
         const float* Tl = T + rep;
 
         for (int64_t r = 0; r < rounds; ++r, ++g) {
-            const int slot = (int)(g % a.nst);
-            mbar_wait(bar0 + 8u * slot, (uint32_t)((g / a.nst) & 1));
+            const uint32_t gq = (uint32_t)g / (uint32_t)a.nst;     // 32-bit: no 64-bit division call
+            const int slot = (int)((uint32_t)g - gq * (uint32_t)a.nst);
+            mbar_wait(bar0 + 8u * slot, gq & 1u);
             const unsigned char* cs = ring + (size_t)slot * K2L_STAGE;
             const int64_t r0 = i0 + r * IPR;
             uint64_t keys[J];

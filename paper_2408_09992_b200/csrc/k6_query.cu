@@ -152,7 +152,7 @@ __global__ void __launch_bounds__(K6_THREADS) k6_query(const K6Args a) {
     stamp(0);
 
     auto issue = [&](int64_t r) {
-        const int slot = (int)(r % a.nst);
+        const int slot = (int)((uint32_t)r % (uint32_t)a.nst);   // rounds < 2^32 per chunk
         const int64_t s0 = i0 + r * IPR;
         const uint32_t bytes = (uint32_t)align_up((size_t)(min((int64_t)IPR, i1 - s0) * MP), 16);
         const uint32_t bar = bar0 + 8u * slot;
