@@ -693,12 +693,14 @@ __global__ void k2_tile_S(const float* __restrict__ S, const uint8_t* __restrict
     const int64_t total = (int64_t)n_groups * m * b * R;
     for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < total;
          x += (int64_t)gridDim.x * blockDim.x) {
-        const int w = (int)(x % R);
-        const int64_t r = x / R;                       // (g, k, c)
-        const int c = (int)(r % b);
-        const int64_t gk = r / b;
-        const int k = (int)(gk % m);
-        const int g = (int)(gk / m);
+        // (g, k, c, w) of x; the table has < 2^32 entries: 32-bit unsigned arithmetic
+        const uint32_t xx = (uint32_t)x;
+        const int w = (int)(xx % (uint32_t)R);
+        const uint32_t r = xx / (uint32_t)R;
+        const int c = (int)(r % (uint32_t)b);
+        const uint32_t gk = r / (uint32_t)b;
+        const int k = (int)(gk % (uint32_t)m);
+        const int g = (int)(gk / (uint32_t)m);
         const int user = g * R + w;
         St[x] = user < B ? S[((int64_t)user * m + k) * b + cmap[k * b + c]] : 0.0f;
     }
@@ -713,10 +715,11 @@ __global__ void k2_tile_S_pair(const float* __restrict__ S, int B, int m, int R,
     const int64_t total = (int64_t)n_groups * rows * R;
     for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < total;
          x += (int64_t)gridDim.x * blockDim.x) {
-        const int w = (int)(x % R);
-        const int64_t r = x / R;
-        const int row = (int)(r % rows);
-        const int g = (int)(r / rows);
+        const uint32_t xx = (uint32_t)x;               // < 2^32 entries
+        const int w = (int)(xx % (uint32_t)R);
+        const uint32_t r = xx / (uint32_t)R;
+        const int row = (int)(r % (uint32_t)rows);
+        const int g = (int)(r / (uint32_t)rows);
         const int user = g * R + w;
         float v = 0.0f;
         if (user < B) {
@@ -867,6 +870,7 @@ void launch_k2_tiled_prep(const pq_index_s* idx, const K2Plan& p, const float* S
     PQ_CUDA(cudaMemsetAsync(gtau_of(idx, p, St), 0, (size_t)p.n_groups * p.G * 8, st));
     const TiledShape sh = k2_tiled_shape(idx->m, idx->b);
     const int64_t total = (int64_t)(st_table_bytes(sh, p.n_groups) / 4);
+    if (total >= ((int64_t)1 << 32)) fail(PQ_ERR_UNSUPPORTED, "tiled tables exceed 2^32 entries (batch too large)");
     const int threads = 256;
     const int blocks = (int)std::min<int64_t>(ceil_div(total, threads), (int64_t)idx->num_sms * 16);
     if (sh.pair) k2_tile_S_pair<<<blocks, threads, 0, st>>>(S, B, idx->m, p.G, p.n_groups, St);

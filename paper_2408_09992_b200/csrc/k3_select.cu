@@ -23,7 +23,7 @@ struct SrcPairs {       // (ids, scores)[p][u][j], e = p*K + j
     const float* sc;
     int B, K;
     __device__ __forceinline__ uint64_t get(int u, int64_t e) const {
-        int p = (int)(e / K), j = (int)(e - (int64_t)p * K);
+        int p = (int)((uint32_t)e / (uint32_t)K), j = (int)(e - (int64_t)p * K);   // e < P * K < 2^32
         int64_t o = ((int64_t)p * B + u) * K + j;
         int32_t id = ids[o];
         if (id < 0) return 0ull;
