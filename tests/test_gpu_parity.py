@@ -379,6 +379,8 @@ FUSED_CASES = [
     (524, 7, 8, 256, 32, 4, 10, "uniform"),            # K > N: padding
     (525, 40_000, 8, 256, 40, 1, 1, "few"),            # ties, K = 1
     (526, 300_007, 16, 200, 128, 4, 64, "zipf"),       # b not a power of 2, ragged tail
+    (527, 2_000_003, 16, 256, 64, 4, 100, "uniform"),  # many chunks per user, 8 table copies
+    (528, 900_001, 8, 256, 256, 2, 50, "zipf"),        # skewed codes, d/m = 32
 ]
 
 
