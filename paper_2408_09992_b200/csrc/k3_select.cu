@@ -81,32 +81,10 @@ k3_select(Src src, int64_t L, int K, int Kp, uint64_t* __restrict__ out_keys,
     if (tid == 0) sh[2] = 0;
     __syncthreads();
 
-    uint64_t kth = 0;
-    if (n > K) {
-        uint64_t prefix = 0;
-        uint32_t krem = (uint32_t)K;
-        for (int shift = 56; shift >= 0; shift -= 8) {
-            const uint64_t hmask = (shift == 56) ? 0ull : (~0ull << (shift + 8));
-            for (int i = tid; i < 256; i += blockDim.x) hist[i] = 0;
-            __syncthreads();
-            for (int i0 = 0; i0 < n; i0 += blockDim.x) {
-                int i = i0 + tid;
-                uint64_t v = i < n ? keys[i] : 0ull;
-                bool ok = (i < n) && ((v & hmask) == prefix);
-                hist_add(hist, ok, (uint32_t)(v >> shift) & 255u);
-            }
-            __syncthreads();
-            if (tid < 32) {
-                uint32_t dg, ab;
-                warp_find_digit(hist, krem, dg, ab);
-                if (tid == 0) { sh[0] = dg; sh[1] = ab; }
-            }
-            __syncthreads();
-            prefix |= (uint64_t)sh[0] << shift;
-            krem -= sh[1];
-        }
-        kth = prefix;
-    }
+    // the K-th largest key: MSD radix select with an early exit once the digit
+    // bin holding it contains exactly the keys still to take (select_dev.cuh)
+    __shared__ unsigned long long sc3[4];
+    const uint64_t kth = n > K ? block_kth(keys, n, (uint32_t)K, hist, sc3) : 0ull;
     // keep keys > kth, plus kth itself when it is a real key (unique); the empty
     // key 0 is never collected (padding is 0 anyway)
     for (int i = tid; i < n; i += blockDim.x) {
