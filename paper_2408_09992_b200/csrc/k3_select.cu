@@ -12,6 +12,7 @@
 namespace pq {
 
 constexpr int K3_THREADS = 512;
+static_assert(K3_SEG >= 2 * PQTOPK_MAX_K, "each merge level must at least halve the candidate list");
 
 struct SrcKeys {        // keys[u][e], row length L
     const uint64_t* keys;

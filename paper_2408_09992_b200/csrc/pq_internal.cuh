@@ -179,7 +179,7 @@ void launch_k2(const pq_index_s* idx, const K2Plan& p, const float* S, int B, in
                uint64_t* lanebuf, uint64_t* cand, cudaStream_t st);
 
 // K3 (k3_select.cu): segmented exact top-K
-constexpr int K3_SEG = 16384;          // keys per K3 block (smem-resident)
+constexpr int K3_SEG = 8192;           // keys per K3 block (smem-resident; 2 blocks per SM; >= 2 PQTOPK_MAX_K so every merge level halves the list)
 size_t k3_reduce_scratch_bytes(int64_t L, int B, int K);
 // keys [B][L] -> ids/scores [B][K] (sorted), multi-level; scratch from above
 void k3_keys_to_topk(const uint64_t* keys, int64_t L, int B, int K, void* scratch,
