@@ -52,9 +52,36 @@ k1_subscores(const float* __restrict__ phi, const float* __restrict__ psi, int B
     for (int t0 = 0; t0 < dm; t0 += K1_TT) {
         const int tt = min(K1_TT, dm - t0);
         __syncthreads();
-        for (int x = threadIdx.x; x < nb * tt; x += K1_THREADS) {
-            int g = x / tt, t = x - g * tt;
-            ps[g * K1_PS + t] = (double)psi[((int64_t)k * b + g0 + g) * dm + t0 + t];
+        if (tt == K1_TT && (dm & 3) == 0) {
+            // full tile, float4-aligned rows: all of a thread's loads are issued
+            // before any conversion (the staging is latency-bound otherwise)
+            constexpr int Q = K1_TT / 4;                // float4 per row
+            const int total = nb * Q;
+            for (int x0 = 0; x0 < total; x0 += 8 * K1_THREADS) {
+                float4 v[8];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    const int x = x0 + i * K1_THREADS + threadIdx.x;
+                    if (x < total) {
+                        const int g = x / Q, c = x - g * Q;
+                        v[i] = __ldg(reinterpret_cast<const float4*>(psi + ((int64_t)k * b + g0 + g) * dm + t0) + c);
+                    }
+                }
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    const int x = x0 + i * K1_THREADS + threadIdx.x;
+                    if (x < total) {
+                        const int g = x / Q, c = x - g * Q;
+                        double* d = ps + g * K1_PS + 4 * c;
+                        d[0] = (double)v[i].x; d[1] = (double)v[i].y; d[2] = (double)v[i].z; d[3] = (double)v[i].w;
+                    }
+                }
+            }
+        } else {
+            for (int x = threadIdx.x; x < nb * tt; x += K1_THREADS) {
+                int g = x / tt, t = x - g * tt;
+                ps[g * K1_PS + t] = (double)psi[((int64_t)k * b + g0 + g) * dm + t0 + t];
+            }
         }
         for (int x = threadIdx.x; x < nu * tt; x += K1_THREADS) {
             int u = x / tt, t = x - u * tt;
