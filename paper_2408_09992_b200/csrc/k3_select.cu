@@ -60,6 +60,33 @@ k3_select(Src src, int64_t L, int K, int Kp, uint64_t* __restrict__ out_keys,
     const int tid = threadIdx.x;
 
     for (int i = tid; i < n; i += blockDim.x) keys[i] = src.get(u, e0 + i);
+    if (n <= (int)blockDim.x) {
+        // very short lists: thread i ranks key i against all (keys are unique; the
+        // empty key 0 ranks last) and writes it straight to its sorted position
+        __syncthreads();
+        const uint64_t mine = tid < n ? keys[tid] : 0ull;
+        int rk = 0;
+#pragma unroll 4
+        for (int j = 0; j < n; ++j) rk += keys[j] > mine ? 1 : 0;
+        const int nz = __syncthreads_count(mine != 0ull);
+        if (mine != 0ull && rk < K) {
+            if (out_ids) {
+                out_ids[(int64_t)u * K + rk] = key_id(mine);
+                out_sc[(int64_t)u * K + rk] = key_score(mine);
+            } else {
+                out_keys[((int64_t)u * out_lists + list_off + s) * K + rk] = mine;
+            }
+        }
+        for (int j = nz + tid; j < K; j += blockDim.x) {
+            if (out_ids) {
+                out_ids[(int64_t)u * K + j] = -1;
+                out_sc[(int64_t)u * K + j] = -INFINITY;
+            } else {
+                out_keys[((int64_t)u * out_lists + list_off + s) * K + j] = 0ull;
+            }
+        }
+        return;
+    }
     if (n <= 1024) {
         // short lists (small batches, the B x P x K merges): sort them whole
         const int P = pow2_ceil(n > 0 ? n : 1);
