@@ -525,7 +525,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--compare", default="auto", choices=["auto", "on", "off"],
                     help="time the paper's baselines beside PQTopK (auto: c2, c3)")
-    ap.add_argument("--variant", type=int, default=0, help="force K2 variant (1, 2 or 3; 0 = auto)")
+    ap.add_argument("--variant", type=int, default=0,
+                    help="force the K2 variant (1 row groups, 2 paired, 3 tiled, 4 small batch; 5 = fused K6 in pq_search; 0 = auto)")
     ap.add_argument("--graph", default="auto", choices=["auto", "on", "off"],
                     help="replay the step as a CUDA graph (auto: single GPU)")
     ap.add_argument("--no-flush", action="store_true", help="diagnostics: skip the L2 flush (not a valid bench line)")
