@@ -749,9 +749,8 @@ static K2TFn tiled_pair_fn(int m_v, int W) {
     if (m_v == 7) return tiled_fn_w<7, 7, 16, 32, 256>(W);
     return nullptr;
 }
-// Instantiated shapes: R = 16 (paired layout) for b = 256, m in {8, 16};
-// R = 32 (item order) when the 32-user table fits: (m, b) in {(4, 16), (8, 16), (4, 256)},
-// and, in phases of 2 splits, b = 256 with m in {32, 64}.
+// Instantiated shapes: R = 16 (paired layout) for b = 256, m in {8, 16, 32, 64};
+// R = 32 (item order) when the 32-user table fits: (m, b) in {(4, 16), (8, 16), (4, 256)}.
 static K2TFn tiled_fn(int m, int b, int R, int W) {
     if (R == 16 && b == 256) {
         if (m == 16) return tiled_fn_w<16, 4, 256, 16>(W);
@@ -762,8 +761,9 @@ static K2TFn tiled_fn(int m, int b, int R, int W) {
         if (m == 8) return tiled_fn_w<8, 8, 16, 32>(W);
     }
     if (R == 32 && b == 256 && m == 4) return tiled_fn_w<4, 4, 256, 32>(W);
-    // many splits (Fig. 2b's m = 64): 16 users in item order (no colour pairing:
-    // 64-split signatures have no complements), phases of 4 splits
+    // many splits (Fig. 2b's m = 64): 16 users, phases of 4 splits; pq_create pairs
+    // items on complementary colours over the first 20 splits (64-split signatures
+    // have no complements), so those splits' gathers are conflict-free
     if (R == 16 && b == 256 && m == 32) return tiled_fn_w<32, 4, 256, 16>(W);
     if (R == 16 && b == 256 && m == 64) return tiled_fn_w<64, 4, 256, 16>(W);
     return nullptr;

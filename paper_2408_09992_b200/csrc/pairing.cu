@@ -49,19 +49,24 @@ PairLayout build_pairing(const uint8_t* codes, int64_t N, int m, int b, int tm) 
             (c == 0 ? m0 : m1) += w;
         }
     }
-    const uint32_t mask = (m >= 32) ? 0xFFFFFFFFu : ((1u << m) - 1u);
+    // Signatures cover the first sm = min(m, 20) splits: with m > 20 (e.g. 64)
+    // exact complements of all splits are essentially absent, but pairs that are
+    // complementary on 20 of them are plentiful and conflict-free on those splits
+    // (about half of the others collide at random either way).
+    const int sm = m < 20 ? m : 20;
+    const uint32_t mask = (1u << sm) - 1u;
     std::vector<uint32_t> sig((size_t)N);
     for (int64_t i = 0; i < N; ++i) {
         uint32_t s = 0;
-        for (int k = 0; k < m; ++k) s |= (uint32_t)color[(size_t)k * 256 + codes[i * m + k]] << k;
+        for (int k = 0; k < sm; ++k) s |= (uint32_t)color[(size_t)k * 256 + codes[i * m + k]] << k;
         sig[i] = s;
     }
     // group item ids by signature (ids ascending inside a group)
     std::vector<int64_t> ids((size_t)N);
     std::vector<int64_t> start;
     std::vector<uint32_t> keys;        // distinct signatures, ascending
-    if (m <= 24) {
-        const size_t nb = (size_t)1 << m;
+    if (sm <= 24) {
+        const size_t nb = (size_t)1 << sm;
         std::vector<int64_t> cnt(nb + 1, 0);
         for (int64_t i = 0; i < N; ++i) cnt[sig[i] + 1]++;
         for (size_t s = 0; s < nb; ++s) cnt[s + 1] += cnt[s];
@@ -100,8 +105,8 @@ PairLayout build_pairing(const uint8_t* codes, int64_t N, int m, int b, int tm) 
     // Second pass over the leftovers: pair items whose signatures differ from
     // each other's complement in ONE split (those pairs conflict on one split
     // only instead of about m/2).  Greedy, in ascending signature order.
-    if (m <= 20 && !left.empty()) {
-        const size_t nb = (size_t)1 << m;
+    if (sm <= 20 && !left.empty()) {
+        const size_t nb = (size_t)1 << sm;
         std::vector<int64_t> head(nb, -1), nxt(left.size(), -1);
         for (size_t t = left.size(); t-- > 0;) {
             const uint32_t sg = sig[left[t]];
@@ -114,7 +119,7 @@ PairLayout build_pairing(const uint8_t* codes, int64_t N, int m, int b, int tm) 
             if (used[t]) continue;
             const uint32_t sg = sig[left[t]];
             int64_t mate = -1;
-            for (int j = 0; j < m && mate < 0; ++j) {
+            for (int j = 0; j < sm && mate < 0; ++j) {
                 const uint32_t c = (sg ^ mask) ^ (1u << j);
                 int64_t& h = head[c];
                 while (h >= 0 && used[h]) h = nxt[h];

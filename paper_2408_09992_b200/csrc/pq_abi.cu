@@ -228,7 +228,7 @@ static void build_v3_layout(pq_index_s* idx, CreateCtx& cx, const uint8_t* codes
     const int mv = sh.m_v;                             // stored splits per row
     PairLayout Lio;
     const PairLayout* Lp = &Lio;
-    if (R == 16 && m <= 20) {
+    if (R == 16) {                                     // colour pairing (m > 20: on 20 splits)
         Lp = &pairing0(cx, idx, codes_in, dev_src, st);
     } else {                                           // item order, codes * (R * 4)
         PairLayout& L = Lio;
@@ -419,8 +419,9 @@ pq_status pq_index_layout(pq_index idx, int32_t* paired, int32_t* tmem_splits,
                           int64_t* pairs_matched, int64_t* leftover_items) {
     PQ_API_BEGIN
     need(idx != nullptr, "index is NULL");
-    // the colour pairing is shared by the v2 and v3 layouts (pq_create)
-    const bool p3 = idx->v3_ok && idx->v3_R == 16 && idx->m <= 20;
+    // the colour pairing is shared by the v2 and v3 layouts (pq_create); for m > 20
+    // it pairs complementary colours on the first 20 splits
+    const bool p3 = idx->v3_ok && idx->v3_R == 16;
     if (paired) *paired = (idx->v2_ok || p3) ? 1 : 0;
     if (tmem_splits) *tmem_splits = idx->v2_ok ? idx->v2_tm : 0;
     if (pairs_matched) *pairs_matched = idx->v2_ok ? idx->v2_matched : (p3 ? idx->v3_matched : 0);
