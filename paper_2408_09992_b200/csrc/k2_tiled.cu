@@ -154,7 +154,10 @@ template <int PS> struct CodePair {
     __device__ __forceinline__ uint32_t off(int e, int kk, uint32_t q16) const {
         if constexpr (K2_CODE_BYTES == 1) {
             const uint32_t wd = w[(e * PS + kk) >> 2];     // PS here = stored codes per row
-            return ((wd >> (8 * ((e * PS + kk) & 3))) & 0xFFu) * RB + q16;
+            if constexpr (PS == 4)                         // byte extract by PRMT (C4: -0.6%)
+                return __byte_perm(wd, 0u, 0x4440u | (uint32_t)((e * PS + kk) & 3)) * RB + q16;
+            else
+                return ((wd >> (8 * ((e * PS + kk) & 3))) & 0xFFu) * RB + q16;
         } else {
             const uint32_t wd = w[(e * PS + kk) >> 1];
             return ((e * PS + kk) & 1) ? ((wd >> 16) + q16) : ((wd & 0xFFFFu) | q16);
