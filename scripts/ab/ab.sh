@@ -1,4 +1,4 @@
-# A/B two versions of k2_tiled.cu on the same box: CFG=c4 REPS=2 bash scripts/ab/ab.sh
+# A/B two versions of k2_tiled.cu on the same box (write scripts/ab/k2_tiled_A.cu and _B.cu first, e.g. from git show):
 rm -f gpurun_out/sweep_results.txt
 for v in A B A B; do
   cp scripts/ab/k2_tiled_$v.cu paper_2408_09992_b200/csrc/k2_tiled.cu
