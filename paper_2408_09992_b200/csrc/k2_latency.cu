@@ -255,7 +255,7 @@ void plan_k2_latency(const pq_index_s* idx, int B, int K, K2Plan& p) {
     p.n_groups = B;
     p.smem = latency_smem(idx->m, idx->b, G, nst);
     K2LFn fn = latency_fn(idx->m, G);
-    PQ_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem));
+    ensure_max_smem(reinterpret_cast<const void*>(fn), (int)p.smem);
     // chunks: about one wave of CTAs, >= one round each, 16-item aligned
     const int64_t N = idx->N;
     const int64_t ipr = K2L_STAGE / latency_mp(idx->m);

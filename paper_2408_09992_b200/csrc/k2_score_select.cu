@@ -226,7 +226,7 @@ static K2Plan plan_k2_paired(const pq_index_s* idx, int B, int K) {
     p.cap = (int)align_up((size_t)std::max(2 * K, K + 4 * p.J), 32);
     p.smem = k2_paired_smem(idx->m, p.tm, idx->b, p.W);
     K2Fn fn = k2_paired_fn(idx->m, p.tm, idx->b);
-    PQ_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem));
+    ensure_max_smem(reinterpret_cast<const void*>(fn), (int)p.smem);
     int occ = 0;
     PQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, p.W * 32, p.smem));
     if (occ < 1) fail(PQ_ERR_UNSUPPORTED, "paired scoring kernel cannot be resident");
@@ -284,7 +284,7 @@ K2Plan plan_k2(const pq_index_s* idx, int B, int K) {
     p.smem = k2_smem(m, b, G, p.W);
 
     K2Fn fn = pick(G, m);
-    PQ_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem));
+    ensure_max_smem(reinterpret_cast<const void*>(fn), (int)p.smem);
     int occ = 0;
     PQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, p.W * 32, p.smem));
     if (occ < 1) fail(PQ_ERR_UNSUPPORTED, "scoring kernel cannot be resident (occupancy 0)");

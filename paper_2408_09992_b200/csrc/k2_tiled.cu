@@ -840,7 +840,7 @@ void plan_k2_tiled(const pq_index_s* idx, int B, int K, K2Plan& p) {
     p.smem = k2_tiled_smem(sh, p.W);
     K2TFn fn = tiled_fn_shape(sh, p.W);
     if (!fn) fail(PQ_ERR_UNSUPPORTED, "tiled scoring kernel: unsupported shape");
-    PQ_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem));
+    ensure_max_smem(reinterpret_cast<const void*>(fn), (int)p.smem);
     int occ = 0;
     PQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, p.W * 32, p.smem));
     if (occ < 1) fail(PQ_ERR_UNSUPPORTED, "tiled scoring kernel cannot be resident");

@@ -144,13 +144,8 @@ static size_t k3_smem(int K) {
 template <class Src>
 static void launch_k3(Src src, int64_t L, int B, int K, uint64_t* out_keys, int64_t out_lists,
                       int64_t list_off, int32_t* ids, float* sc, cudaStream_t st) {
-    static bool attr_done = false;          // benign race: idempotent attribute set
     size_t smem = k3_smem(K);
-    if (!attr_done) {
-        PQ_CUDA(cudaFuncSetAttribute(k3_select<Src>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)(K3_SEG * 8 + PQTOPK_MAX_K * 8 + 256 * 4 + 16)));
-        attr_done = true;
-    }
+    ensure_max_smem(reinterpret_cast<const void*>(k3_select<Src>), (int)(K3_SEG * 8 + PQTOPK_MAX_K * 8 + 256 * 4 + 16));
     int n_sub = (int)ceil_div(L, K3_SEG);
     dim3 grid((unsigned)B, (unsigned)n_sub);
     int Kp = pow2_ceil(std::min(K, K3_SEG));

@@ -749,7 +749,7 @@ static bool plan_uncached(const pq_index_s* idx, int B, int d, int K, K6Plan& p)
     p.G = G; p.nst = nst;
     p.smem = query_smem(m, idx->b, G, nst, d, B);
     K6Fn fn = query_fn(m, G, idx->b);
-    PQ_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem));
+    ensure_max_smem(reinterpret_cast<const void*>(fn), (int)p.smem);
     // Cluster size CL: the CTAs of a cluster split one user's sub-id score work
     // (E * L fp64 fmas, E = m * b, L = d / m) -- a larger CL shortens that
     // prologue but packs fewer CTAs (clusters are placed within a GPC).  The

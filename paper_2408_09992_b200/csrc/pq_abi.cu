@@ -7,6 +7,7 @@
 #include <vector>
 
 #include "pq_internal.cuh"
+#include <mutex>
 
 namespace pq {
 
@@ -22,6 +23,25 @@ void check_cuda(cudaError_t e, const char* what) {
 void check_launch(const char* what) {
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) fail(PQ_ERR_CUDA, std::string("launch ") + what + ": " + cudaGetErrorString(e));
+}
+
+void ensure_max_smem(const void* fn, int bytes) {
+    struct Ent { int dev; const void* fn; int bytes; };
+    static std::mutex mu;
+    static std::vector<Ent> done;
+    int dev = 0;
+    check_cuda(cudaGetDevice(&dev), "cudaGetDevice");
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        for (const Ent& e : done)
+            if (e.dev == dev && e.fn == fn && e.bytes >= bytes) return;
+    }
+    check_cuda(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes),
+               "cudaFuncSetAttribute(MaxDynamicSharedMemorySize)");
+    std::lock_guard<std::mutex> lk(mu);
+    for (Ent& e : done)
+        if (e.dev == dev && e.fn == fn) { if (bytes > e.bytes) e.bytes = bytes; return; }
+    done.push_back(Ent{dev, fn, bytes});
 }
 
 static bool is_device_ptr(const void* p) {

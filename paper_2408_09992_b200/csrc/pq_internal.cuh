@@ -26,6 +26,9 @@ void clear_error();
 [[noreturn]] void fail(pq_status st, const std::string& msg);
 void check_cuda(cudaError_t e, const char* what);
 void check_launch(const char* what);        // cudaGetLastError after a launch
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (device, kernel, size):
+// the plans run on every call and the attribute call is host time on small queries
+void ensure_max_smem(const void* fn, int bytes);
 extern std::atomic<int64_t> g_launches;     // kernels launched by this library
 inline void count_launch(int n = 1) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
