@@ -512,3 +512,26 @@ def test_create_destroy_frees_device_memory(pq, torch):
     torch.cuda.synchronize()
     free1 = torch.cuda.mem_get_info()[0]
     assert free0 - free1 < (8 << 20), (free0, free1)
+
+
+def test_search_plan_and_flags(pq, torch):
+    """pq_search_plan_info reports the fused kernel for B <= 4 and the batched
+    K2 plan otherwise; unknown pq_search_ex flags are rejected."""
+    import ctypes
+    G, P, F = pqsynth.random_instance(710, 100_000, 8, 256, 64, 8)
+    idx = pq.pq_create(G, b=256)
+    assert idx.search_plan(1, 64, 10)["variant"] == 5
+    assert idx.search_plan(8, 64, 10)["variant"] == idx.plan(8, 10)["variant"]
+    idx.set_tuning(variant=4)                          # K2 v4 forced: pq_search runs K1 + v4 + K3
+    assert idx.search_plan(1, 64, 10)["variant"] == 4
+    idx.set_tuning()
+    L = pq.load_library()
+    Fd, Pd = cuda(torch, F[:1]), cuda(torch, P)
+    ids = torch.empty((1, 10), dtype=torch.int32, device="cuda")
+    sc = torch.empty((1, 10), dtype=torch.float32, device="cuda")
+    nb = int(L.pq_search_workspace_bytes(idx.handle, 1, 64, 10))
+    ws = torch.empty(nb, dtype=torch.uint8, device="cuda")
+    st = L.pq_search_ex(idx.handle, ctypes.c_void_p(Fd.data_ptr()), ctypes.c_void_p(Pd.data_ptr()), 1, 64, 10,
+                        0x100, ctypes.c_void_p(ws.data_ptr()), nb, ctypes.c_void_p(ids.data_ptr()),
+                        ctypes.c_void_p(sc.data_ptr()), None, None)
+    assert st != 0 and b"flags" in L.pq_last_error()
