@@ -121,6 +121,19 @@ def dist_env():
     return world, rank, local
 
 
+def launched_by_torchrun() -> bool:
+    """Under torch.distributed.run (WORLD_SIZE set) the sharded path runs --
+    process group, packed all-gather and merge -- even at world size 1."""
+    return "WORLD_SIZE" in os.environ
+
+
+def parity_users(B: int, n: int = 64):
+    """Users checked against the oracle: n users spread evenly over the batch
+    (stride B/n), so every user group / CTA tile of the batch is sampled."""
+    n = min(n, B)
+    return sorted({(j * B) // n for j in range(n)})
+
+
 def shard(N, world, rank):
     from paper_2408_09992_b200.dist import shard_range
     return shard_range(N, world, rank)
@@ -133,22 +146,43 @@ def workload_name(cfg):
 
 def cpu_oracle_sample(cfg, codes, S_host, gpu_ids, gpu_sc, budget_s=12.0, max_users=64):
     """Time the CPU oracle (Alg. 1, plain C + OpenMP) on a bounded sample of
-    users over the full catalogue; also check those users bit-exactly."""
+    users over the full catalogue -- users spread over the whole batch
+    (parity_users) -- and check those users bit-exactly against the GPU result.
+    Also times one user with ONE thread (the per-core figure)."""
     import oracle
-    done, t_tot, exact = 0, 0.0, 0
-    while done < min(max_users, cfg.B) and t_tot < budget_s:
-        u = done
+    users = parity_users(cfg.B, max_users)
+    done, t_tot, exact, checked = 0, 0.0, 0, []
+    for u in users:
+        if t_tot >= budget_s:
+            break
         t0 = time.perf_counter()
         ids, sc = oracle.pq_topk(codes, S_host[u:u + 1], cfg.K)
         t_tot += time.perf_counter() - t0
         if gpu_ids is not None:
             exact += int(np.array_equal(ids[0], gpu_ids[u]) and
                          np.array_equal(sc[0].view(np.uint32), gpu_sc[u].view(np.uint32)))
+        checked.append(u)
         done += 1
-    return {"value": done * cfg.N / t_tot, "unit": "user-item scores/s", "cores": oracle.max_threads(),
-            "kind": "oracle",
-            "sample": f"users 0..{done - 1} of {cfg.B} over all {cfg.N:,} items (Alg. 1 item-major, "
-                      f"fp32 k-ordered sums, heap top-K), {t_tot:.1f} s"}, done, exact
+    cores = oracle.max_threads()
+    # one thread, one user (bounded: about 2e8 lookups, ~1 s)
+    n1 = min(cfg.N, max(1, int(2e8 // max(cfg.m, 1))))
+    oracle.set_threads(1)
+    try:
+        t0 = time.perf_counter()
+        oracle.pq_topk(codes[:n1], S_host[:1], cfg.K)
+        t1 = time.perf_counter() - t0
+    finally:
+        oracle.set_threads(cores)
+    stride = (cfg.B // len(users)) if users else 0
+    desc = (f"users {checked[0]}..{checked[-1]} step {stride} ({done} of {cfg.B})" if done > 1
+            else f"user {checked[0]} of {cfg.B}")
+    cpu = {"value": done * cfg.N / t_tot, "unit": "user-item scores/s", "cores": cores,
+           "kind": "oracle", "cpu_model": oracle.cpu_model(),
+           "sample": f"{desc} over all {cfg.N:,} items (Alg. 1 item-major, fp32 k-ordered sums, "
+                     f"heap top-K), {t_tot:.1f} s",
+           "one_thread": {"value": n1 / t1, "unit": "user-item scores/s",
+                          "sample": f"user 0 over items 0..{n1 - 1:,}, 1 thread, {t1:.2f} s"}}
+    return cpu, checked, exact
 
 
 # ----------------------------------------------------------------------------- reference arm
@@ -181,7 +215,7 @@ def run_reference(args):
     value = upstep * cfg.N / t
     line = {
         "impl": "reference", "metric": "user-item scores/s", "value": value, "unit": "user-item scores/s",
-        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
+        "n_gpus": max(world, args.gpus), "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f32", "data": "synthetic (pqsynth, seeded)",
         "config": {"workload": workload_name(cfg), "users_per_step": upstep},
@@ -241,15 +275,21 @@ def run_ours(args):
     import paper_2408_09992_b200 as pq
 
     world, rank, local = dist_env()
+    sharded = launched_by_torchrun()
+    if torch.cuda.device_count() <= local:
+        raise SystemExit(f"bench.py: rank {rank} needs cuda:{local} but only "
+                         f"{torch.cuda.device_count()} GPU(s) are visible")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
+    if sharded:
         dist.init_process_group("nccl", device_id=dev)
     pq.load_library()
     cfg = pqsynth.CONFIGS[args.config]
     B, K, m, b, d = cfg.B, cfg.K, cfg.m, cfg.b, cfg.d
     lo, hi = shard(cfg.N, world, rank)
     n_local = hi - lo
+    if n_local <= 0:
+        raise SystemExit(f"bench.py: {cfg.name} has fewer items ({cfg.N}) than ranks ({world})")
 
     codes = pqsynth.codes(cfg, lo, hi)
     P = pqsynth.psi(cfg)
@@ -272,26 +312,29 @@ def run_ours(args):
     plan = idx.search_plan(B, d, K) if fused else idx.plan(B, K)
     layout = idx.layout()
 
+    from paper_2408_09992_b200.dist import alloc_local, gather_merge
+
     F_d = torch.from_numpy(F).to(dev)
     P_d = torch.from_numpy(P).to(dev)
     S = torch.empty((B, m, b), dtype=torch.float32, device=dev)
-    ids = torch.empty((B, K), dtype=torch.int32, device=dev)
-    sc = torch.empty((B, K), dtype=torch.float32, device=dev)
+    # the local result is written straight into the packed [2][B][K] buffer the
+    # all-gather sends (plane 0 ids, plane 1 score bits)
+    packed, ids, sc = alloc_local(B, K, dev)
     ws = torch.empty(idx.topk_workspace_bytes(B, K), dtype=torch.uint8, device=dev)
     sws = torch.empty(idx.search_workspace_bytes(B, d, K), dtype=torch.uint8, device=dev)
-    if world > 1:
+    if sharded:
         out_ids = torch.empty((B, K), dtype=torch.int32, device=dev)
         out_sc = torch.empty((B, K), dtype=torch.float32, device=dev)
+        gbuf = torch.empty((world * 2, B, K), dtype=torch.int32, device=dev)
         mws_n = int(pq.load_library().pq_merge_workspace_bytes(world, B, K))
         mws = torch.empty(max(mws_n, 1), dtype=torch.uint8, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     if args.no_flush:                                # diagnostics only: the line is marked invalid
         flush = torch.empty(0, dtype=torch.uint8, device=dev)
 
-    from paper_2408_09992_b200.dist import gather_merge
-
-    def merge_into_out(gi, gs):
-        return pq.pq_merge_topk(gi, gs, ws=mws, out_ids=out_ids, out_scores=out_sc)
+    def exchange():
+        # ONE NCCL all-gather of the packed B x K (id, score) pairs + pq_merge_topk_packed (dist.py)
+        gather_merge(packed, out=(out_ids, out_sc), ws=mws, gathered=gbuf)
 
     def step():
         if fused:
@@ -299,11 +342,11 @@ def run_ours(args):
         else:
             pq.pq_subscores(F_d, P_d, S)
             pq.pq_score_topk(idx, S, K, ws=ws, ids=ids, scores=sc)
-        if world > 1:                                # NCCL all-gather of B x K + merge (dist.py)
-            gather_merge(ids, sc, merge=merge_into_out)
+        if sharded:
+            exchange()
 
     def barrier():
-        if world > 1:
+        if sharded:
             dist.barrier()
 
     for _ in range(args.warmup):
@@ -315,7 +358,7 @@ def run_ours(args):
     # removes host launch gaps, which dominate the small configs).  The fused
     # kernel's own launch time for the roofline is measured in a separate
     # non-graph pass with the library's per-launch events.
-    use_graph = args.graph == "on" or (args.graph == "auto" and world == 1)
+    use_graph = args.graph == "on" or (args.graph == "auto" and not sharded)
     graph = None
     if use_graph:
         side = torch.cuda.Stream()
@@ -355,7 +398,7 @@ def run_ours(args):
     # codes fit in it (SURVEY §8(d) L2 policy: report warm and cold)
     warm_ms = None
     l2_bytes = torch.cuda.get_device_properties(dev).L2_cache_size
-    if world == 1 and n_local * m < l2_bytes:
+    if not sharded and n_local * m < l2_bytes:
         evw = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                for _ in range(args.steps)]
         for e0, e1 in evw:
@@ -377,7 +420,7 @@ def run_ours(args):
     k2_ms, k3_ms, n_k2 = idx.timing_read()
     idx.timing_enable(False)
     t = torch.tensor([tot_ms, k2_ms], dtype=torch.float64, device=dev)
-    if world > 1:
+    if sharded:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     tot_ms_max, k2_ms_max = float(t[0]), float(t[1])
     ms_per_step = tot_ms_max / args.steps
@@ -390,11 +433,11 @@ def run_ours(args):
     sc_h = torch.empty((B, K), dtype=torch.float32).pin_memory()
 
     def e2e_step():
-        if world == 1:
+        if not sharded:
             pq.pq_search(idx, F_h, P_h, K, ws=sws, ids=ids_h, scores=sc_h)
-        else:
+        else:                                        # host inputs -> local result -> exchange -> host
             pq.pq_search(idx, F_h, P_h, K, ws=sws, ids=ids, scores=sc)
-            gather_merge(ids, sc, merge=merge_into_out)
+            exchange()
             ids_h.copy_(out_ids, non_blocking=True)
             sc_h.copy_(out_sc, non_blocking=True)
     for _ in range(max(1, args.warmup)):
@@ -412,19 +455,21 @@ def run_ours(args):
     barrier()
     e2e_ms = sum(a.elapsed_time(c) for a, c in evs2)
     t2 = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
-    if world > 1:
+    if sharded:
         dist.all_reduce(t2, op=dist.ReduceOp.MAX)
     e2e_value = B * cfg.N / (float(t2[0]) / args.steps / 1e3)
 
     # final results for parity sampling (rank 0 at N = 1); the fused kernel's own S
     if fused:
         pq.pq_search(idx, F_d, P_d, K, ws=sws, ids=ids, scores=sc, S_out=S)
+        if sharded:
+            exchange()
     torch.cuda.synchronize()
-    res_ids = (out_ids if world > 1 else ids).cpu().numpy()
-    res_sc = (out_sc if world > 1 else sc).cpu().numpy()
+    res_ids = (out_ids if sharded else ids).cpu().numpy()
+    res_sc = (out_sc if sharded else sc).cpu().numpy()
 
     if rank != 0:
-        if world > 1:
+        if sharded:
             dist.barrier()
             dist.destroy_process_group()
         return
@@ -475,13 +520,19 @@ def run_ours(args):
                     "unit": "GB/s", "frac": (hbm_bytes / k2_avg_s) / peak_hbm, **common}
     cpu = None
     parity = None
-    if world == 1 and not args.no_cpu_baseline:
-        cpu, nu, nexact = cpu_oracle_sample(cfg, codes, S.cpu().numpy(), res_ids, res_sc)
-        parity = f"bit-exact vs oracle (given GPU S) on {nexact}/{nu} sampled users"
+    if not args.no_cpu_baseline:
+        # rank 0 checks the MERGED global result against the oracle over the
+        # WHOLE catalogue (at N > 1 it regenerates the other shards' codes)
+        full_codes = codes if world == 1 else pqsynth.codes(cfg)
+        cpu, users, nexact = cpu_oracle_sample(cfg, full_codes, S.cpu().numpy(), res_ids, res_sc)
+        del full_codes
+        parity = (f"bit-exact vs oracle (given GPU S) on {nexact}/{len(users)} sampled users "
+                  f"(users {users[0]}..{users[-1]}, stride {cfg.B // max(1, len(parity_users(cfg.B)))}"
+                  f"{', merged over ' + str(world) + ' shards' if sharded else ''})")
     clocks = sampler.summary()
     comparison = None
     want_cmp = args.compare == "on" or (args.compare == "auto" and cfg.name in ("c2", "c3"))
-    if world == 1 and want_cmp and cfg.N * d * 4 <= (48 << 30):
+    if not sharded and want_cmp and cfg.N * d * 4 <= (48 << 30):
         comparison = compare_paths(pq, torch, idx, cfg, F_d, P_d, S, step, flush, ms_per_step)
     line = {
         "metric": "user-item scores/s", "value": value, "unit": "user-item scores/s",
@@ -490,7 +541,8 @@ def run_ours(args):
         "vs_baseline": None, "dtype": "f32", "data": "synthetic (pqsynth, seeded; BASELINE.json config recipe)",
         "config": {"workload": workload_name(cfg), "items_per_gpu": n_local,
                    "k2_plan": plan, "layout": layout,
-                   "parallelism": f"item-shard x{world}" if world > 1 else "single GPU",
+                   "parallelism": (f"item-shard x{world} (NCCL all-gather of packed B x K pairs + "
+                                   "pq_merge_topk_packed)") if sharded else "single GPU",
                    "cuda_graph": graph is not None,
                    "l2": ("NO L2 flush (diagnostic run, not a bench value)" if args.no_flush else
                           "256 MiB L2 flush before every timed step (outside events)")},
@@ -510,9 +562,27 @@ def run_ours(args):
                     "warm_l2_median": warm_ms},
     }
     print(json.dumps(line), flush=True)
-    if world > 1:
+    if sharded:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def relaunch_torchrun(n: int) -> int:
+    import socket
+    import subprocess
+
+    import torch
+    have = torch.cuda.device_count()
+    if have < n:
+        print(f"bench.py: --gpus {n} needs {n} visible GPUs, found {have}", file=sys.stderr)
+        return 1
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
 
 
 def main():
@@ -536,6 +606,16 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("bench.py: --warmup must be >= 3", file=sys.stderr)
+    if args.gpus < 1:
+        raise SystemExit("bench.py: --gpus must be >= 1")
+    if launched_by_torchrun():
+        ws_env = int(os.environ["WORLD_SIZE"])
+        if ws_env != args.gpus:
+            raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws_env}; "
+                             "launch one rank per GPU (torch.distributed.run --nproc-per-node N)")
+    elif args.gpus > 1 and args.impl == "ours":
+        # not under torchrun: re-launch this command as N ranks, one per GPU
+        sys.exit(relaunch_torchrun(args.gpus))
     if args.impl == "reference":
         run_reference(args)
     else:

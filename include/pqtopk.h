@@ -32,8 +32,12 @@
  *   * device faults surface at the next synchronising call as PQ_ERR_CUDA;
  *   * the library never allocates on the hot path: scratch memory is the
  *     caller's `ws` of at least the size the *_workspace_bytes call returns;
- *     concurrent calls need distinct workspaces; a pq_index is immutable and
- *     may be shared across threads and streams.
+ *     concurrent calls need distinct workspaces; a pq_index's catalogue is
+ *     immutable and the index may be shared across threads and streams by the
+ *     compute calls.  The configuration calls pq_set_tuning and
+ *     pq_timing_enable mutate the index and are NOT thread-safe: call them
+ *     while no other thread uses the index (timing records themselves are
+ *     mutex-protected).
  */
 #ifndef PQTOPK_H
 #define PQTOPK_H
@@ -75,8 +79,11 @@ typedef struct {
     int32_t users_per_row; /* G, table row width in users (0 = auto; power of 2, <= 32) */
     int32_t shrink_watermark; /* K2 v3 candidate-buffer shrink watermark (0 = automatic; tests
                                  use a small value to force frequent shrinks) */
-    int32_t cluster;     /* K6: CTAs per thread-block cluster sharing one user's sub-id
-                            score computation (0 = auto (4); 1, 2, 4 or 8) */
+    int32_t cluster;     /* K6 prologue mode: 0 = cooperative GRID mode when B users' CTAs fit
+                            in one wave (sub-id scores shared through L2 behind a grid
+                            barrier), else cluster mode with a modelled cluster size;
+                            1, 2, 4 or 8 = CLUSTER mode with that many CTAs per
+                            thread-block cluster sharing one user's sub-id scores */
     int32_t reserved[1];
 } pq_tuning;
 
@@ -266,16 +273,33 @@ size_t pq_merge_workspace_bytes(int32_t P, int32_t B, int32_t K);
 
 /*
  * pq_merge_topk — merge P partial top-K lists per user (e.g. the allgathered
- * local results of P item shards) into the global top-K.
+ * local results of P item shards) into the global top-K (TopK of Alg. 1,
+ * P:125, over the union of the shards' item sets; item loop sharded as P:122/
+ * P:129 allow).
  *   ids, scores : [P][B][K], device; entries with id < 0 are empty.
  *   out_ids, out_scores : [B][K], device, outputs (same contract as
  *                         pq_score_topk).  Inputs must not alias outputs.
+ * PRECONDITION: a real id appears in at most one of the P lists of a user
+ * (the lists come from disjoint item shards).  Repeated ids are not detected;
+ * the call stays memory-safe and writes every output slot, but the output may
+ * then contain the repeated id twice.
  * Because every shard's list is its exact local top-K under the same total
  * order, the merge equals the unsharded result bit for bit.
  */
 pq_status pq_merge_topk(const int32_t* ids, const float* scores, int32_t P,
                         int32_t B, int32_t K, void* ws, size_t ws_bytes,
                         int32_t* out_ids, float* out_scores, void* stream);
+
+/*
+ * pq_merge_topk_packed — pq_merge_topk over ONE packed buffer, the layout a
+ * single all-gather of the shards' (id, score) pairs produces:
+ *   lists : int32 [P][2][B][K], device: plane 0 = ids, plane 1 = the fp32
+ *           score bits.  Same precondition, workspace
+ *           (pq_merge_workspace_bytes) and outputs as pq_merge_topk.
+ */
+pq_status pq_merge_topk_packed(const int32_t* lists, int32_t P, int32_t B, int32_t K,
+                               void* ws, size_t ws_bytes, int32_t* out_ids,
+                               float* out_scores, void* stream);
 
 /*
  * pq_reconstruct — dense item embeddings (Eq. 2):

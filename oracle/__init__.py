@@ -51,6 +51,7 @@ def lib():
         P, I32, I64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64
         L.orc_check_fpenv.restype = ctypes.c_int
         L.orc_max_threads.restype = ctypes.c_int
+        L.orc_set_threads.argtypes = [ctypes.c_int]
         L.orc_subscores64.argtypes = [P, P, I64, I32, I32, I32, P, P]
         L.orc_scores_alg1.argtypes = [P, I64, I32, I32, P, P]
         L.orc_scores_alg2.argtypes = [P, I64, I32, I32, P, P]
@@ -81,6 +82,21 @@ def _c(a, dt):
 
 def max_threads() -> int:
     return int(lib().orc_max_threads())
+
+
+def set_threads(n: int) -> None:
+    """OpenMP thread count for later calls (results are thread-count invariant)."""
+    lib().orc_set_threads(int(n))
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 # ---------------------------------------------------------------------------

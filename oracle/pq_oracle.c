@@ -41,6 +41,16 @@ int orc_max_threads(void) {
 #endif
 }
 
+/* Thread count for the following calls (plumbing for the 1-thread timing; the
+ * results do not depend on it: test_thread_count_invariance). */
+void orc_set_threads(int n) {
+#ifdef _OPENMP
+    if (n > 0) omp_set_num_threads(n);
+#else
+    (void)n;
+#endif
+}
+
 /* ---------------------------------------------------------------------------
  * Eq. 4: s_{k,j} = psi_{k,j} . phi_k, with phi_k the k-th contiguous
  * d/m chunk of phi (R10).  S64[u][k][g] in fp64, t ascending; C holds the

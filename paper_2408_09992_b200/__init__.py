@@ -19,6 +19,7 @@ from .binding import (  # noqa: F401
     pq_create,
     pq_dense_topk,
     pq_merge_topk,
+    pq_merge_topk_packed,
     pq_recjpq_topk,
     pq_reconstruct,
     pq_score_topk,
@@ -32,6 +33,6 @@ from . import dist  # noqa: F401,E402  (item sharding across GPUs)
 
 __all__ = [
     "PQError", "PQIndex", "Tuning", "abi_version", "launch_count", "lib_path", "load_library",
-    "pq_create", "pq_subscores", "pq_score_topk", "pq_score_topk_subset", "pq_score_topk_exclude", "pq_search", "pq_merge_topk",
+    "pq_create", "pq_subscores", "pq_score_topk", "pq_score_topk_subset", "pq_score_topk_exclude", "pq_search", "pq_merge_topk", "pq_merge_topk_packed",
     "pq_reconstruct", "pq_dense_topk", "pq_recjpq_topk",
 ]

@@ -27,7 +27,7 @@ MAX_K = 4096
 EXPORTS = ["pq_abi_version", "pq_last_error", "pq_launch_count", "pq_create", "pq_create_ex", "pq_destroy",
            "pq_index_info", "pq_index_layout", "pq_index_variants", "pq_plan_info", "pq_set_tuning", "pq_subscores", "pq_topk_workspace_bytes",
            "pq_score_topk", "pq_search_workspace_bytes", "pq_search", "pq_search_ex", "pq_search_plan_info", "pq_merge_workspace_bytes",
-           "pq_merge_topk", "pq_reconstruct", "pq_dense_workspace_bytes", "pq_dense_topk",
+           "pq_merge_topk", "pq_merge_topk_packed", "pq_reconstruct", "pq_dense_workspace_bytes", "pq_dense_topk",
            "pq_recjpq_workspace_bytes", "pq_recjpq_topk", "pq_timing_enable", "pq_timing_read",
            "pq_subset_workspace_bytes", "pq_score_topk_subset", "pq_exclude_workspace_bytes",
            "pq_score_topk_exclude"]
@@ -89,6 +89,7 @@ def load_library():
         "pq_search_plan_info": (st, [P, I32, I32, I32, ctypes.POINTER(I64)]),
         "pq_merge_workspace_bytes": (SZ, [I32, I32, I32]),
         "pq_merge_topk": (st, [P, P, I32, I32, I32, P, SZ, P, P, P]),
+        "pq_merge_topk_packed": (st, [P, I32, I32, I32, P, SZ, P, P, P]),
         "pq_reconstruct": (st, [P, P, I32, P, P]),
         "pq_dense_workspace_bytes": (SZ, [I64, I32, I32]),
         "pq_dense_topk": (st, [P, I64, I32, P, I32, I32, I64, P, SZ, P, P, P]),
@@ -410,6 +411,29 @@ def pq_merge_topk(ids, scores, ws=None, out_ids=None, out_scores=None, stream=No
                            ctypes.c_void_p(_ptr(ws) if ws is not None else 0), wsb,
                            ctypes.c_void_p(_ptr(out_ids)), ctypes.c_void_p(_ptr(out_scores)),
                            ctypes.c_void_p(_stream(stream))))
+    return out_ids, out_scores
+
+
+def pq_merge_topk_packed(lists, ws=None, out_ids=None, out_scores=None, stream=None):
+    """Merge the packed int32 [P][2][B][K] lists (plane 0 ids, plane 1 fp32
+    score bits) that ONE all-gather of the shards' results produces into [B][K]."""
+    torch = _torch()
+    _need_cuda(lists, "lists")
+    if lists.dtype != torch.int32 or lists.dim() != 4 or int(lists.shape[1]) != 2:
+        raise ValueError("lists must be int32 [P][2][B][K]")
+    P, _, B, K = (int(x) for x in lists.shape)
+    dev = lists.device
+    if out_ids is None:
+        out_ids = torch.empty((B, K), dtype=torch.int32, device=dev)
+    if out_scores is None:
+        out_scores = torch.empty((B, K), dtype=torch.float32, device=dev)
+    L = load_library()
+    nb = int(L.pq_merge_workspace_bytes(P, B, K))
+    ws, wsb = _ws(nb, ws, dev)
+    _check(L.pq_merge_topk_packed(ctypes.c_void_p(_ptr(lists)), P, B, K,
+                                  ctypes.c_void_p(_ptr(ws) if ws is not None else 0), wsb,
+                                  ctypes.c_void_p(_ptr(out_ids)), ctypes.c_void_p(_ptr(out_scores)),
+                                  ctypes.c_void_p(_stream(stream))))
     return out_ids, out_scores
 
 

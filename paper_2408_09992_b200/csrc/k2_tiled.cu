@@ -77,8 +77,8 @@ struct K2TArgs {
     int n_groups, chunks;
     int64_t chunk_tiles;       // tiles per item chunk
     uint64_t* ubuf;            // [grid][R][cap] per-user candidate buffers
-    int cap;                   // >= 2K + 2 TR + 96 (see the shrink protocol)
-    int wm;                    // shrink watermark (<= cap - 2 TR - 32)
+    int cap;                   // >= 2K + 3 TR + 96 (see the shrink protocol)
+    int wm;                    // shrink watermark (<= cap - 3 TR - 32)
     uint64_t* cand;            // [B][chunks][K]
     unsigned long long* gtau;  // [n_groups * R] per-user proved thresholds (zeroed per call)
     long long* trace;          // diagnostics (PQTOPK_K2_TRACE): CTA 0 phase timeline, or null
@@ -361,8 +361,11 @@ __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
     // Shrink protocol (no per-tile barrier): the insert that takes a user's
     // buffer to `wm` entries during tile T records T + 1 in sflag[T & 1]; at
     // the end of tile T + 1 every warp (having waited until all warps finished
-    // tile T) sees the same flag and the CTA shrinks.  Between the request and
-    // the shrink at most 2 * TR more entries arrive: cap >= wm + 2 * TR.
+    // tile T) sees the same flag and the CTA shrinks.  Warps drift by up to one
+    // tile (a warp passes the end of tile T once all warps finished T - 1), so
+    // when a warp in tile T makes the request, slower warps may still insert
+    // the rest of tile T - 1; with tiles T and T + 1 that is at most 3 * TR
+    // entries per user before the shrink: cap >= wm + 3 * TR.
     const int wm = a.wm;
     int64_t tseq = 0;                                  // tiles done by this CTA
 
@@ -559,7 +562,7 @@ __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
                                 if (!(cmask >> (4 * d + j) & 1u) || !(vv[j] >= tf[j])) continue;
                                 const int u = 4 * q + j;
                                 const int p = atomicAdd(&cnt_u[u], 1);
-                                if (p >= a.cap) __trap();      // protocol invariant: cap >= wm + 2 TR
+                                if (p >= a.cap) __trap();      // protocol invariant: cap >= wm + 3 TR
                                 ubuf[(int64_t)u * a.cap + p] = make_raw(vv[j] + 0.0f, row);
                                 if (p == wm) {
                                     *reinterpret_cast<volatile int*>(&sflag[tseq & 1]) = (int)(tseq + 1);
@@ -836,7 +839,7 @@ void plan_k2_tiled(const pq_index_s* idx, int B, int K, K2Plan& p) {
     p.tm = (sh.m_v / sh.ps) > 1 ? sh.m_v - sh.ps : 0;
     p.n_groups = (int)ceil_div(B, R);
     const int TR = k2_tiled_rows_per_tile(R);
-    p.cap = (int)align_up((size_t)(2 * K + 2 * TR + 96), 32);
+    p.cap = (int)align_up((size_t)(2 * K + 3 * TR + 96), 32);
     p.smem = k2_tiled_smem(sh, p.W);
     K2TFn fn = tiled_fn_shape(sh, p.W);
     if (!fn) fail(PQ_ERR_UNSUPPORTED, "tiled scoring kernel: unsupported shape");
@@ -896,7 +899,7 @@ void launch_k2_tiled(const pq_index_s* idx, const K2Plan& p, int B, int K,
     a.ubuf = lanebuf; a.cap = p.cap; a.cand = cand;
     {
         const int TR = k2_tiled_rows_per_tile(p.G);
-        const int wmax = p.cap - 2 * TR - 32;
+        const int wmax = p.cap - 3 * TR - 32;
         const int tw = idx->tuning.shrink_watermark;
         a.wm = tw > 0 ? std::min(std::max(tw, K + 1), wmax) : wmax;
     }

@@ -19,13 +19,14 @@ struct SrcKeys {        // keys[u][e], row length L
     int64_t L;
     __device__ __forceinline__ uint64_t get(int u, int64_t e) const { return keys[(int64_t)u * L + e]; }
 };
-struct SrcPairs {       // (ids, scores)[p][u][j], e = p*K + j
+struct SrcPairs {       // (ids, scores)[p][u][j] at p*pstride + u*K + j, e = p*K + j
     const int32_t* ids;
     const float* sc;
-    int B, K;
+    int64_t pstride;    // elements between consecutive lists (B*K plain, 2*B*K packed)
+    int K;
     __device__ __forceinline__ uint64_t get(int u, int64_t e) const {
         int p = (int)((uint32_t)e / (uint32_t)K), j = (int)(e - (int64_t)p * K);   // e < P * K < 2^32
-        int64_t o = ((int64_t)p * B + u) * K + j;
+        int64_t o = (int64_t)p * pstride + (int64_t)u * K + j;
         int32_t id = ids[o];
         if (id < 0) return 0ull;
         return make_key(sc[o] + 0.0f, (uint32_t)id);     // + 0.0f: -0 -> +0 (R2)
@@ -66,8 +67,11 @@ k3_select(Src src, int64_t L, int K, int Kp, uint64_t* __restrict__ out_keys,
         __syncthreads();
         const uint64_t mine = tid < n ? keys[tid] : 0ull;
         int rk = 0;
+        // keys are unique for valid inputs; the index tie-break only keeps the
+        // output slots distinct (memory-safe, every slot written) if a caller
+        // passes a repeated (id, score) pair, which the contract forbids
 #pragma unroll 4
-        for (int j = 0; j < n; ++j) rk += keys[j] > mine ? 1 : 0;
+        for (int j = 0; j < n; ++j) rk += (keys[j] > mine || (keys[j] == mine && j < tid)) ? 1 : 0;
         const int nz = __syncthreads_count(mine != 0ull);
         if (mine != 0ull && rk < K) {
             if (out_ids) {
@@ -119,7 +123,7 @@ k3_select(Src src, int64_t L, int K, int Kp, uint64_t* __restrict__ out_keys,
         uint64_t v = keys[i];
         if (v != 0ull && v >= kth) {
             uint32_t pos = atomicAdd(&sh[2], 1u);
-            sel[pos] = v;
+            if (pos < (uint32_t)Kp) sel[pos] = v;    // > K only with repeated input keys (caller error)
         }
     }
     __syncthreads();
@@ -189,11 +193,11 @@ size_t k3_pairs_scratch_bytes(int P, int B, int K) {
     return first + k3_reduce_scratch_bytes(n_sub * K, B, K);
 }
 
-void k3_pairs_to_topk(const int32_t* ids_in, const float* sc_in, int P, int B, int K,
-                      void* scratch, int32_t* ids, float* scores, cudaStream_t st) {
+void k3_pairs_to_topk(const int32_t* ids_in, const float* sc_in, int64_t pstride, int P, int B,
+                      int K, void* scratch, int32_t* ids, float* scores, cudaStream_t st) {
     if (B <= 0 || K <= 0) return;
     int64_t L = (int64_t)P * K;
-    SrcPairs src{ids_in, sc_in, B, K};
+    SrcPairs src{ids_in, sc_in, pstride, K};
     if (L <= K3_SEG) {
         launch_k3(src, L, B, K, nullptr, 0, 0, ids, scores, st);
         return;

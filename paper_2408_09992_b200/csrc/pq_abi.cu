@@ -110,6 +110,7 @@ static void run_score_topk(pq_index_s* idx, const float* S, int B, int K, void* 
     k3_keys_to_topk(cand, (int64_t)w.plan.chunks * K, B, K, k3s, ids, scores, st);
     if (idx->timing) {
         PQ_CUDA(cudaEventRecord(ev.c, st));
+        std::lock_guard<std::mutex> lk(*idx->ev_mu);
         idx->events->push_back(ev);
     }
 }
@@ -419,6 +420,7 @@ pq_status pq_destroy(pq_index idx) {
     if (idx->events) {
         for (auto& e : *idx->events) { cudaEventDestroy(e.a); cudaEventDestroy(e.b); cudaEventDestroy(e.c); }
         delete idx->events;
+        delete idx->ev_mu;
     }
     k6_cache_free(idx);
     delete idx;
@@ -598,6 +600,7 @@ pq_status pq_search_ex(pq_index idx, const float* seq_emb, const float* subitem_
         if (idx->timing) {
             PQ_CUDA(cudaEventRecord(ev.b, st));
             PQ_CUDA(cudaEventRecord(ev.c, st));
+            std::lock_guard<std::mutex> lk(*idx->ev_mu);
             idx->events->push_back(ev);
         }
     } else {
@@ -645,7 +648,24 @@ pq_status pq_merge_topk(const int32_t* ids, const float* scores, int32_t P, int3
     const size_t nb = pq_merge_workspace_bytes(P, B, K);
     if (nb && (!ws || ws_bytes < nb))
         fail(PQ_ERR_WORKSPACE, "workspace too small: need " + std::to_string(nb) + " bytes");
-    k3_pairs_to_topk(ids, scores, P, B, K, ws, out_ids, out_scores, static_cast<cudaStream_t>(stream));
+    k3_pairs_to_topk(ids, scores, (int64_t)B * K, P, B, K, ws, out_ids, out_scores,
+                     static_cast<cudaStream_t>(stream));
+    PQ_API_END
+}
+
+pq_status pq_merge_topk_packed(const int32_t* lists, int32_t P, int32_t B, int32_t K, void* ws,
+                               size_t ws_bytes, int32_t* out_ids, float* out_scores, void* stream) {
+    PQ_API_BEGIN
+    need(P >= 1, "P must be >= 1");
+    check_topk_args(B, K);
+    if (B == 0 || K == 0) return PQ_OK;
+    need(lists && out_ids && out_scores, "NULL pointer");
+    const size_t nb = pq_merge_workspace_bytes(P, B, K);
+    if (nb && (!ws || ws_bytes < nb))
+        fail(PQ_ERR_WORKSPACE, "workspace too small: need " + std::to_string(nb) + " bytes");
+    const int64_t BK = (int64_t)B * K;
+    k3_pairs_to_topk(lists, reinterpret_cast<const float*>(lists + BK), 2 * BK, P, B, K, ws, out_ids,
+                     out_scores, static_cast<cudaStream_t>(stream));
     PQ_API_END
 }
 
@@ -817,8 +837,11 @@ pq_status pq_score_topk_exclude(pq_index idx, const float* S, int32_t B, int32_t
 pq_status pq_timing_enable(pq_index idx, int32_t on) {
     PQ_API_BEGIN
     need(idx != nullptr, "index is NULL");
+    if (on && !idx->events) {
+        idx->ev_mu = new std::mutex();
+        idx->events = new std::vector<pq_index_s::EvTriple>();
+    }
     idx->timing = on ? 1 : 0;
-    if (on && !idx->events) idx->events = new std::vector<pq_index_s::EvTriple>();
     PQ_API_END
 }
 
@@ -828,6 +851,7 @@ pq_status pq_timing_read(pq_index idx, double* k2_ms, double* k3_ms, int64_t* la
     double t2 = 0.0, t3 = 0.0;
     int64_t n = 0;
     if (idx->events) {
+        std::lock_guard<std::mutex> lk(*idx->ev_mu);
         for (auto& e : *idx->events) {
             float a = 0.f, c = 0.f;
             PQ_CUDA(cudaEventSynchronize(e.c));

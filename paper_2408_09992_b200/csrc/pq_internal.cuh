@@ -8,6 +8,7 @@
 #include <string>
 #include <atomic>
 #include <algorithm>
+#include <mutex>
 #include <vector>
 
 #include "../../include/pqtopk.h"
@@ -109,6 +110,7 @@ struct pq_index_s {
     int timing = 0;
     struct EvTriple { cudaEvent_t a, b, c; };
     std::vector<EvTriple>* events = nullptr;
+    std::mutex* ev_mu = nullptr;   // guards `events` (calls may come from several threads)
 };
 
 namespace pq {
@@ -189,8 +191,8 @@ void k3_keys_to_topk(const uint64_t* keys, int64_t L, int B, int K, void* scratc
                      int32_t* ids, float* scores, cudaStream_t st);
 // pairs [P][B][K] -> ids/scores [B][K]
 size_t k3_pairs_scratch_bytes(int P, int B, int K);
-void k3_pairs_to_topk(const int32_t* ids_in, const float* sc_in, int P, int B, int K,
-                      void* scratch, int32_t* ids, float* scores, cudaStream_t st);
+void k3_pairs_to_topk(const int32_t* ids_in, const float* sc_in, int64_t pstride, int P, int B,
+                      int K, void* scratch, int32_t* ids, float* scores, cudaStream_t st);
 // score rows R[B][ld] (cols [0,n)) -> keys appended at out[u][list_off .. ) in
 // lists of K; returns the number of lists written per user
 int k3_rows_lists(int64_t n);

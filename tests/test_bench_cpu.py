@@ -9,10 +9,10 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def _run(env_extra):
+def _run(env_extra, gpus=1):
     env = dict(os.environ, **env_extra)
     r = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--config", "c1",
-                        "--steps", "2", "--warmup", "1"], cwd=ROOT, env=env,
+                        "--steps", "2", "--warmup", "1", "--gpus", str(gpus)], cwd=ROOT, env=env,
                        capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stderr[-2000:]
     return [json.loads(x) for x in r.stdout.splitlines() if x.startswith("{")]
@@ -33,4 +33,20 @@ def test_reference_arm_line():
 
 
 def test_reference_arm_non_zero_rank_is_silent():
-    assert _run({"RANK": "1", "WORLD_SIZE": "2", "LOCAL_RANK": "1"}) == []
+    assert _run({"RANK": "1", "WORLD_SIZE": "2", "LOCAL_RANK": "1"}, gpus=2) == []
+
+
+def test_gpus_flag_is_not_ignored():
+    """--gpus N without torchrun re-launches N ranks; with fewer visible GPUs it
+    fails loudly instead of benchmarking one GPU; a --gpus / WORLD_SIZE mismatch
+    is refused."""
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    env["CUDA_VISIBLE_DEVICES"] = ""
+    r = subprocess.run([sys.executable, "bench.py", "--gpus", "2", "--config", "c1", "--steps", "3"],
+                       cwd=ROOT, env=env, capture_output=True, text=True, timeout=300)
+    assert r.returncode != 0 and "needs 2 visible GPUs" in r.stderr, r.stderr[-1000:]
+    assert not any(x.startswith("{") for x in r.stdout.splitlines())
+    env2 = dict(env, WORLD_SIZE="2", RANK="0", LOCAL_RANK="0")
+    r = subprocess.run([sys.executable, "bench.py", "--gpus", "1", "--config", "c1"], cwd=ROOT,
+                       env=env2, capture_output=True, text=True, timeout=300)
+    assert r.returncode != 0 and "WORLD_SIZE=2" in r.stderr, r.stderr[-1000:]

@@ -209,11 +209,19 @@ def test_merge_large_p(pq, torch, orc):
 
 
 def test_recjpq_gpu_bitwise(pq, torch, orc):
-    """Alg. 2 on the GPU == Alg. 1 fused kernel, bitwise."""
-    G, P, F = pqsynth.random_instance(140, 70_001, 8, 256, 64, 9)
-    S, ids, sc, idx = run_pq(pq, torch, G, P, F, 50)
-    ri, rs = pq.pq_recjpq_topk(idx, cuda(torch, S), 50)
-    assert_same(ri.cpu().numpy(), rs.cpu().numpy(), ids, sc)
+    """Alg. 2 (RecJPQScore) on the GPU == the oracle's Alg. 2 AND
+    Alg. 1 given the same S, bit for bit (equivalence A)."""
+    for seed, N, m, b, B, K, dist in ((140, 70_001, 8, 256, 9, 50, "uniform"),
+                                      (141, 33_333, 4, 16, 3, 700, "uniform"),   # ties
+                                      (142, 5_000, 3, 64, 2, 6_000, "zipf")):    # K > N
+        G, P, F = pqsynth.random_instance(seed, N, m, b, 4 * m, B, code_dist=dist)
+        idx = pq.pq_create(G, b=b, id_base=7)
+        S_t = pq.pq_subscores(cuda(torch, F), cuda(torch, P))
+        ri, rs = pq.pq_recjpq_topk(idx, S_t, K)
+        S_h = S_t.cpu().numpy()
+        oi, os_ = orc.recjpq_topk(G, S_h, K, id_base=7)
+        assert_same(ri.cpu().numpy(), rs.cpu().numpy(), oi, os_, str(seed))
+        assert_same(oi, os_, *orc.pq_topk(G, S_h, K, id_base=7), str(seed))
 
 
 def test_dense_path(pq, torch, orc):
@@ -242,17 +250,48 @@ def test_dense_path(pq, torch, orc):
 
 
 def test_search_host_buffers(pq, torch, orc):
-    """pq_search with host (pinned) inputs/outputs == device path."""
-    G, P, F = pqsynth.random_instance(160, 80_000, 8, 256, 64, 12)
-    S, ids, sc, idx = run_pq(pq, torch, G, P, F, 30)
-    Fh = torch.from_numpy(F).pin_memory()
-    Ph = torch.from_numpy(P).pin_memory()
-    oi = torch.empty((12, 30), dtype=torch.int32).pin_memory()
-    os_ = torch.empty((12, 30), dtype=torch.float32).pin_memory()
-    pq.pq_search(idx, Fh, Ph, 30, ids=oi, scores=os_)
-    assert_same(oi.numpy(), os_.numpy(), ids, sc)
-    di, ds = pq.pq_search(idx, cuda(torch, F), cuda(torch, P), 30)
-    assert_same(di.cpu().numpy(), ds.cpu().numpy(), ids, sc)
+    """pq_search with host (pinned) inputs/outputs -- the call bench.py's e2e
+    times -- and with device buffers, both against the oracle given the S the
+    library computes (and the multi-kernel host-staging path: B = 12 > 4)."""
+    for seed, N, B, K in ((160, 80_000, 12, 30), (161, 50_001, 3, 10), (162, 20_011, 40, 100)):
+        G, P, F = pqsynth.random_instance(seed, N, 8, 256, 64, B)
+        idx = pq.pq_create(G, b=256)
+        Fh = torch.from_numpy(F).pin_memory()
+        Ph = torch.from_numpy(P).pin_memory()
+        oi = torch.empty((B, K), dtype=torch.int32).pin_memory()
+        os_ = torch.empty((B, K), dtype=torch.float32).pin_memory()
+        S_t = torch.empty((B, 8, 256), dtype=torch.float32, device="cuda")
+        pq.pq_search(idx, Fh, Ph, K, ids=oi, scores=os_, S_out=S_t)
+        torch.cuda.synchronize()
+        S_h = S_t.cpu().numpy()
+        assert check_S(orc, F, P, S_h) == 0
+        ref = orc.pq_topk(G, S_h, K)
+        assert_same(oi.numpy(), os_.numpy(), *ref, str(seed))
+        di, ds = pq.pq_search(idx, cuda(torch, F), cuda(torch, P), K)
+        assert_same(di.cpu().numpy(), ds.cpu().numpy(), *ref, str(seed))
+
+
+def test_packed_merge_equals_oracle(pq, torch, orc):
+    """The multi-GPU exchange layout: shard results written into packed
+    [2][B][K] buffers (dist.alloc_local), stacked as ONE all-gather would
+    deliver them ([P][2][B][K]) and merged by pq_merge_topk_packed == the
+    oracle over the whole catalogue; includes an empty (padding) shard."""
+    from paper_2408_09992_b200.dist import alloc_local, fill_empty, shard_range
+    G, P, F = pqsynth.random_instance(133, 90_001, 8, 256, 64, 24)
+    K = 100
+    S_t = pq.pq_subscores(cuda(torch, F), cuda(torch, P))
+    for world in (2, 5):
+        bufs = []
+        for r in range(world):
+            lo, hi = shard_range(G.shape[0], world, r)
+            packed, li, ls = alloc_local(24, K, S_t.device)
+            pq.pq_score_topk(pq.pq_create(G[lo:hi], b=256, id_base=lo), S_t, K, ids=li, scores=ls)
+            bufs.append(packed)
+        e, _, _ = alloc_local(24, K, S_t.device)
+        fill_empty(e)
+        bufs.append(e)
+        mi, ms = pq.pq_merge_topk_packed(torch.stack(bufs))
+        assert_same(mi.cpu().numpy(), ms.cpu().numpy(), *orc.pq_topk(G, S_t.cpu().numpy(), K), str(world))
 
 
 def test_invariants_and_launch_count(pq, torch, orc):
@@ -321,6 +360,10 @@ TILED_CASES = [
     (308, 5_003, 4, 16, 40, 3000, "uniform"),        # K close to N, ties
     (309, 60_001, 64, 256, 40, 100, "uniform"),      # m = 64 (Fig. 2b): R = 32, 32 phases of 2 splits
     (310, 30_011, 32, 256, 33, 500, "zipf"),         # m = 32
+    # all-ties stress of the shrink protocol's capacity (cap >= wm + 3 TR):
+    # 2^m distinct tuples, K = 4000, every tile floods the buffers at the threshold
+    (311, 400_003, 8, 256, 16, 4000, "few"),
+    (312, 200_003, 16, 256, 16, 4000, "few"),        # m = 16: TMEM phases
 ]
 
 
