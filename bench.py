@@ -164,8 +164,8 @@ def cpu_oracle_sample(cfg, codes, S_host, gpu_ids, gpu_sc, budget_s=12.0, max_us
         checked.append(u)
         done += 1
     cores = oracle.max_threads()
-    # one thread, one user (bounded: about 2e8 lookups, ~1 s)
-    n1 = min(cfg.N, max(1, int(2e8 // max(cfg.m, 1))))
+    # one thread, one user (bounded: about 2e9 lookups, ~1 s)
+    n1 = min(cfg.N, max(1, int(2e9 // max(cfg.m, 1))))
     oracle.set_threads(1)
     try:
         t0 = time.perf_counter()
@@ -493,7 +493,7 @@ def run_ours(args):
         hbm_bytes = n_local * m + B * d * 4 + b * d * 4 + B * K * 8
     peak_hbm = pk["hbm_gbs"] * 1e9
     t_smem, t_hbm = lookups / peak_lookups, hbm_bytes / peak_hbm
-    kname = {1: "k2_score_select (v1 row groups)", 2: "k2_paired (v2)",
+    kname = {1: "k2_score_select (v1 row groups)",
              3: "k2_tiled (v3: fused gather-sum-select, 4 users/lane)",
              4: "k2_latency (v4: small-batch fused gather-sum-select)",
              5: "k6_query (K1 + gather-sum + select + merge in one launch, B <= 4)"}.get(plan["variant"], "k2")
@@ -596,7 +596,7 @@ def main():
     ap.add_argument("--compare", default="auto", choices=["auto", "on", "off"],
                     help="time the paper's baselines beside PQTopK (auto: c2, c3)")
     ap.add_argument("--variant", type=int, default=0,
-                    help="force the K2 variant (1 row groups, 2 paired, 3 tiled, 4 small batch; 5 = fused K6 in pq_search; 0 = auto)")
+                    help="force the K2 variant (1 row groups, 3 tiled, 4 small batch; 5 = fused K6 in pq_search; 0 = auto)")
     ap.add_argument("--graph", default="auto", choices=["auto", "on", "off"],
                     help="replay the step as a CUDA graph (auto: single GPU)")
     ap.add_argument("--no-flush", action="store_true", help="diagnostics: skip the L2 flush (not a valid bench line)")

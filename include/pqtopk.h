@@ -68,7 +68,8 @@ typedef enum {
 /* Optional launch tuning (all 0 = automatic).  Any setting gives bit-identical
  * results; this exists for tests (F12: two geometries, same bits) and tuning. */
 typedef struct {
-    int32_t variant;     /* 0 auto; 1 = generic row-group kernel; 2 = paired half-warps;
+    int32_t variant;     /* 0 auto; 1 = generic row-group kernel; (2 = removed: the
+                            superseded paired half-warp kernel; treated as auto);
                             3 = tiled phases (4 users per lane, TMA tables, TMEM partials);
                             4 = small-batch latency kernel (B <= 4, lane = item);
                             pq_search only: 5 = the fused single-launch query kernel (K6,
@@ -119,9 +120,6 @@ pq_status pq_create(const uint8_t* codes, int64_t N, int32_t m, int32_t b,
  *     layouts and their host-side colour pairing — for latency-serving
  *     indexes and very large catalogues (e.g. 10^9 items). */
 #define PQ_CREATE_SMALL_BATCH_ONLY 1
-/*   PQ_CREATE_WITH_V2: also build the layout of the superseded K2 v2 kernel
- *     (paired half-warps with two TMEM splits), kept for comparison tests. */
-#define PQ_CREATE_WITH_V2 2
 pq_status pq_create_ex(const uint8_t* codes, int64_t N, int32_t m, int32_t b,
                        int64_t id_base, int32_t flags, void* stream, pq_index* out);
 
@@ -134,9 +132,9 @@ pq_status pq_index_info(pq_index idx, int64_t* N, int32_t* m, int32_t* b,
 
 /*
  * Layout of an index (diagnostics; any output may be NULL):
- *   paired      : 1 if a colour-paired layout (K2 v3 with 16 users, or v2) was built
- *   tmem_splits : splits of the v2 layout served from tensor memory (0 or 2; 0
- *                 when v2 was not built)
+ *   paired      : 1 if the colour-paired layout (K2 v3 with 16 users) was built
+ *   tmem_splits : always 0 (kept for ABI stability: it described the removed
+ *                 v2 kernel's TMEM-resident splits)
  *   pairs_matched / leftover_items : complementary pairs found / items paired
  *                 without a complement (they are scored correctly but may hit
  *                 shared-memory bank conflicts)

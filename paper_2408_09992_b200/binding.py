@@ -16,7 +16,10 @@ from typing import Optional, Tuple
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-_LIB_PATH = os.path.join(HERE, "libpqtopk.so")
+# PQTOPK_CHECKED=1 loads the checked diagnostics build (device-side bounds
+# checks, bounded waits: `python -m paper_2408_09992_b200.build --checked`)
+_LIB_PATH = os.path.join(HERE, "libpqtopk_checked.so" if os.environ.get("PQTOPK_CHECKED") == "1"
+                         else "libpqtopk.so")
 _lib = None
 
 PQ_STATUS = {0: "PQ_OK", 1: "PQ_ERR_INVALID_ARG", 2: "PQ_ERR_CODE_RANGE", 3: "PQ_ERR_NONFINITE",
@@ -198,7 +201,7 @@ class PQIndex:
                 "leftover_items": lo.value}
 
     def variants(self):
-        """Set of K2 scoring variants this index supports (1 generic, 2 paired, 3 tiled,
+        """Set of K2 scoring variants this index supports (1 generic, 3 tiled,
         4 small-batch latency)."""
         m = ctypes.c_int32()
         _check(load_library().pq_index_variants(self._h, ctypes.byref(m)))
@@ -249,14 +252,11 @@ class PQIndex:
 
 
 SMALL_BATCH_ONLY = 1
-WITH_V2 = 2
 
 
-def pq_create(codes, b: int, id_base: int = 0, stream=None, small_batch_only: bool = False,
-              with_v2: bool = False) -> PQIndex:
+def pq_create(codes, b: int, id_base: int = 0, stream=None, small_batch_only: bool = False) -> PQIndex:
     """Build an index from codes uint8 [N][m] (numpy / CPU tensor / CUDA tensor).
-    small_batch_only: skip the batched layouts (B <= 4 serving / huge catalogues);
-    with_v2: also build the superseded v2 kernel's layout (comparison tests)."""
+    small_batch_only: skip the batched layouts (B <= 4 serving / huge catalogues)."""
     L = load_library()
     if isinstance(codes, np.ndarray):
         codes = np.ascontiguousarray(codes, dtype=np.uint8)
@@ -265,7 +265,7 @@ def pq_create(codes, b: int, id_base: int = 0, stream=None, small_batch_only: bo
     N, m = int(codes.shape[0]), int(codes.shape[1])
     h = ctypes.c_void_p()
     _check(L.pq_create_ex(ctypes.c_void_p(_ptr(codes)), N, m, int(b), int(id_base),
-                          (SMALL_BATCH_ONLY if small_batch_only else 0) | (WITH_V2 if with_v2 else 0),
+                          SMALL_BATCH_ONLY if small_batch_only else 0,
                           ctypes.c_void_p(_stream(stream)), ctypes.byref(h)))
     return PQIndex(h.value, N, m, int(b), int(id_base))
 

@@ -8,22 +8,17 @@ namespace pq {
 
 struct K2Args {
     const uint8_t* codes;      // v1: [N][mp] natural order
-    const uint16_t* codes16;   // v2: [rows][m] pre-shifted stored codes (c' * 64), pair order
-    const int32_t* perm;       // v2: row -> local id (-1 = padding row)
-    const uint8_t* cmap;       // v2: [m][b] stored code -> original code
-    const uint8_t* pos;        // v2: [m][b] original code -> stored code
+    const int32_t* perm;       // row -> local id (-1 = padding row), or null (item order)
     const float* S;            // [B][m][b]
-    int64_t N;                 // v1: items; v2: rows (pairs * 2)
+    int64_t N;                 // items
     int m, b, mp;
     int B, K;
     uint32_t id_base;
     int Ug, n_groups, chunks;
-    int64_t chunk_items;       // v1: items per chunk; v2: pairs per chunk
+    int64_t chunk_items;       // items per chunk
     uint64_t* lanebuf;         // [grid][W][32][cap]
     int cap;
     uint64_t* cand;            // [B][chunks][K]
-    int tmem_splits;           // v2: trailing splits served from tensor memory (0 or 2)
-    uint32_t* ghist;           // v2: [grid][W][256] flush histograms (global scratch)
     uint64_t* mscr;            // [grid][32 * W * K] end-of-unit merge scratch
 };
 

@@ -266,7 +266,7 @@ void plan_k2_latency(const pq_index_s* idx, int B, int K, K2Plan& p) {
     const int64_t units = (int64_t)B * p.chunks;
     p.grid = (int)std::min<int64_t>(units, t.ctas > 0 ? t.ctas : (int64_t)idx->num_sms);
     p.cap = 0;
-    p.lanebuf_bytes = 0; p.mscr_bytes = 0; p.ghist_bytes = 0; p.st_bytes = 0;
+    p.lanebuf_bytes = 0; p.mscr_bytes = 0; p.st_bytes = 0;
     p.cand_bytes = (size_t)B * p.chunks * K * 8;
 }
 

@@ -196,8 +196,6 @@ static size_t k2_smem(int m, int b, int G, int W) {
     return align_up((size_t)m * b * G * 4, 16) + (size_t)W * 256 * 4 + 32 * 8 + 64 * 4;
 }
 
-K2Fn k2_paired_fn(int m, int tm, int b);
-
 static int choose_chunks(int64_t n_items, int n_groups, int grid_full, int64_t min_items) {
     const int64_t max_c = std::max<int64_t>(1, std::min<int64_t>(4096, n_items / min_items));
     int best = 1;
@@ -210,46 +208,6 @@ static int choose_chunks(int64_t n_items, int n_groups, int grid_full, int64_t m
         if (eff >= 0.97) break;
     }
     return best;
-}
-
-static K2Plan plan_k2_paired(const pq_index_s* idx, int B, int K) {
-    K2Plan p;
-    const pq_tuning& t = idx->tuning;
-    p.variant = 2;
-    p.tm = idx->v2_tm;
-    p.W = k2_paired_warps(idx->m, p.tm, idx->b);
-    p.J = 4;
-    const int D = k2_paired_depth(idx->m, p.tm, idx->b);
-    p.G = 16;
-    p.Ug = 16;
-    p.n_groups = (int)ceil_div(B, 16);
-    p.cap = (int)align_up((size_t)std::max(2 * K, K + 4 * p.J), 32);
-    p.smem = k2_paired_smem(idx->m, p.tm, idx->b, p.W);
-    K2Fn fn = k2_paired_fn(idx->m, p.tm, idx->b);
-    ensure_max_smem(reinterpret_cast<const void*>(fn), (int)p.smem);
-    int occ = 0;
-    PQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, p.W * 32, p.smem));
-    if (occ < 1) fail(PQ_ERR_UNSUPPORTED, "paired scoring kernel cannot be resident");
-    if (p.tm > 0) occ = 1;                      // one TMEM allocation of 512 columns per SM
-    const size_t per_cta = (size_t)p.W * 32 * p.cap * 8 + (size_t)32 * p.W * K * 8;
-    const int occ_mem = (int)std::max<size_t>(1, ((size_t)2 << 30) / (per_cta * idx->num_sms));
-    occ = std::min(occ, occ_mem);
-    const int grid_full = idx->num_sms * occ;
-    const int64_t npairs = idx->v2_rows / 2;
-    p.chunks = t.chunks > 0 ? t.chunks : choose_chunks(npairs, p.n_groups, grid_full, 1 << 14);
-    // whole CTA steps per unit (no loop tail); the overhang reads padding rows
-    const int64_t quantum = (int64_t)p.W * p.J * D;
-    p.chunk_items = (int64_t)align_up((size_t)ceil_div(npairs, p.chunks), (size_t)quantum);
-    p.chunks = (int)ceil_div(npairs, p.chunk_items);
-    if ((int64_t)p.chunks * p.chunk_items - npairs + (int64_t)D * p.W * p.J > V2_PAD_ROWS / 2)
-        fail(PQ_ERR_UNSUPPORTED, "internal: chunk overhang exceeds the padding rows");
-    const int64_t units = (int64_t)p.n_groups * p.chunks;
-    p.grid = (int)std::min<int64_t>(units, t.ctas > 0 ? t.ctas : grid_full);
-    p.lanebuf_bytes = (size_t)p.grid * p.W * 32 * p.cap * 8;
-    p.cand_bytes = (size_t)B * p.chunks * K * 8;
-    p.ghist_bytes = (size_t)p.grid * p.W * 256 * 4;
-    p.mscr_bytes = (size_t)p.grid * 32 * p.W * K * 8;
-    return p;
 }
 
 K2Plan plan_k2(const pq_index_s* idx, int B, int K) {
@@ -265,8 +223,6 @@ K2Plan plan_k2(const pq_index_s* idx, int B, int K) {
         plan_k2_latency(idx, B, K, p);
         return p;
     }
-    if (idx->v2_ok && tt.variant != 1 && tt.users_per_row == 0 && (B >= 16 || tt.variant == 2))
-        return plan_k2_paired(idx, B, K);
     K2Plan p;
     const int m = idx->m, b = idx->b;
     const pq_tuning& t = idx->tuning;
@@ -309,27 +265,6 @@ K2Plan plan_k2(const pq_index_s* idx, int B, int K) {
 void launch_k2(const pq_index_s* idx, const K2Plan& p, const float* S, int B, int K,
                uint64_t* lanebuf, uint64_t* cand, cudaStream_t st) {
     K2Args a{};
-    if (p.variant == 2) {
-        a.codes16 = idx->d_codes16;
-        a.perm = idx->d_perm16;
-        a.cmap = idx->d_cmap16;
-        a.pos = idx->d_pos16;
-        a.S = S;
-        a.N = idx->v2_rows;
-        a.m = idx->m; a.b = idx->b; a.mp = idx->m;
-        a.B = B; a.K = K;
-        a.id_base = (uint32_t)idx->id_base;
-        a.Ug = 16; a.n_groups = p.n_groups; a.chunks = p.chunks; a.chunk_items = p.chunk_items;
-        a.lanebuf = lanebuf; a.cap = p.cap; a.cand = cand;
-        a.tmem_splits = p.tm;
-        a.ghist = reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(lanebuf) + align_up(p.lanebuf_bytes, 256));
-        a.mscr = reinterpret_cast<uint64_t*>(reinterpret_cast<char*>(a.ghist) + align_up(p.ghist_bytes, 256));
-        K2Fn fn = k2_paired_fn(idx->m, p.tm, idx->b);
-        fn<<<p.grid, p.W * 32, p.smem, st>>>(a);
-        count_launch();
-        check_launch("k2_paired");
-        return;
-    }
     a.codes = idx->d_codes;
     a.perm = idx->lay.paired ? idx->d_perm : nullptr;
     a.S = S;
@@ -339,8 +274,7 @@ void launch_k2(const pq_index_s* idx, const K2Plan& p, const float* S, int B, in
     a.id_base = (uint32_t)idx->id_base;
     a.Ug = p.Ug; a.n_groups = p.n_groups; a.chunks = p.chunks; a.chunk_items = p.chunk_items;
     a.lanebuf = lanebuf; a.cap = p.cap; a.cand = cand;
-    a.mscr = reinterpret_cast<uint64_t*>(reinterpret_cast<char*>(lanebuf) + align_up(p.lanebuf_bytes, 256) +
-                                         align_up(p.ghist_bytes, 256));
+    a.mscr = reinterpret_cast<uint64_t*>(reinterpret_cast<char*>(lanebuf) + align_up(p.lanebuf_bytes, 256));
     K2Fn fn = pick(p.G, idx->m);
     fn<<<p.grid, p.W * 32, p.smem, st>>>(a);
     count_launch();

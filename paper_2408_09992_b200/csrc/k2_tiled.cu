@@ -69,6 +69,7 @@ int k2_tiled_code_bytes() { return K2_CODE_BYTES; }
 
 struct K2TArgs {
     const void* codes;         // phase-blocked codes (see above), K2_CODE_BYTES each
+    int64_t codes_bytes;       // allocated bytes of `codes` (checked builds bound every load)
     const int32_t* perm;       // [tiles * TR] row -> local id (-1 = padding)
     const float* St;           // [n_groups][m][b][R] tiled sub-score tables
     int64_t n_tiles;           // tiles in the catalogue
@@ -135,6 +136,13 @@ template <int PS> struct CodePair {
     static constexpr int BYTES = 2 * PS * K2_CODE_BYTES;     // per lane per slot pair
     static constexpr int NW = BYTES / 4;
     uint32_t w[NW];
+#ifdef PQTOPK_CHECKED
+    static __device__ __forceinline__ void check(const char* p, const char* base, int64_t nbytes) {
+        PQ_DCHECK(p >= base && p + BYTES <= base + nbytes);
+    }
+#else
+    static __device__ __forceinline__ void check(const char*, const char*, int64_t) {}
+#endif
     __device__ __forceinline__ void load(const char* p) {
         if constexpr (NW == 1) {
             w[0] = __ldg(reinterpret_cast<const uint32_t*>(p));
@@ -413,6 +421,8 @@ __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
 #pragma unroll 1
                 for (int s2 = 0; s2 < SL / 4; s2 += 2) {       // a quarter of the tile suffices
                     CodePair<PSS> cpair;
+                    CodePair<PSS>::check(cp + (int64_t)(s2 / 2) * 2 * RPS * CB,
+                                         reinterpret_cast<const char*>(a.codes), a.codes_bytes);
                     cpair.load(cp + (int64_t)(s2 / 2) * 2 * RPS * CB);
 #pragma unroll
                     for (int e = 0; e < 2; ++e) {
@@ -475,7 +485,10 @@ __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
                                  ((int64_t)warp * SL * RPS + (lane / LPR) * 2)) * CB;
                 CodePair<PSS> cw[DP];
 #pragma unroll
-                for (int d = 0; d < DP; ++d) cw[d].load(cp + d * PSTR);
+                for (int d = 0; d < DP; ++d) {
+                    CodePair<PSS>::check(cp + d * PSTR, reinterpret_cast<const char*>(a.codes), a.codes_bytes);
+                    cw[d].load(cp + d * PSTR);
+                }
                 cp += DP * PSTR;
                 uint32_t tcur[4] = {0u, 0u, 0u, 0u};   // partial sums of slot s (ph > 0)
                 if (ph > 0) {
@@ -493,9 +506,12 @@ __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
                     float4 vb[2][PS];
                     auto gather = [&](int d, float4 (&dst)[PS]) {
 #pragma unroll
-                        for (int kk = 0; kk < PS; ++kk)
+                        for (int kk = 0; kk < PS; ++kk) {
+                            PQ_DCHECK(split_off(kk) + cw[d >> 1].template off<RB>(d & 1, kk, q16) + 16 <= TBLB);
                             dst[kk] = lds128(tb + split_off(kk) + cw[d >> 1].template off<RB>(d & 1, kk, q16));
+                        }
                         if (d & 1) {                   // both slots of the pair addressed: refill
+                            CodePair<PSS>::check(cp, reinterpret_cast<const char*>(a.codes), a.codes_bytes);
                             cw[d >> 1].load(cp);       // DP pairs ahead (buffer is padded)
                             cp += PSTR;
                         }
@@ -608,6 +624,7 @@ __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
             for (long long spins = 0;; ++spins) {
                 const int td = lane < W ? *reinterpret_cast<volatile int*>(&tiles_done[lane]) : INT_MAX;
                 if (__all_sync(FULL, td >= (int)tseq)) break;
+                PQ_DCHECK(spins < PQ_SPIN_LIMIT);      // checked builds: a lost warp traps
                 __nanosleep(64);                       // back off: spinning would steal smem cycles
                 if (a.dbg && spins > (1ll << 26)) {
                     if (lane == 0 && atomicAdd(&a.dbg[0], 1) == 0) {
@@ -660,6 +677,7 @@ __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
         }
         for (int u = warp; u < n_valid; u += W) {
             const int gu = grp * R + u;
+            PQ_DCHECK(gu < a.B && chunk < a.chunks && cnt_u[u] <= a.cap);
             uint64_t* out = a.cand + ((int64_t)gu * a.chunks + chunk) * a.K;
             uint64_t* ub = ubuf + (int64_t)u * a.cap;
             int nn;
@@ -861,7 +879,6 @@ void plan_k2_tiled(const pq_index_s* idx, int B, int K, K2Plan& p) {
     p.grid = (int)std::min<int64_t>(units, t.ctas > 0 ? t.ctas : grid_full);
     p.lanebuf_bytes = (size_t)p.grid * R * p.cap * 8;
     p.cand_bytes = (size_t)B * p.chunks * K * 8;
-    p.ghist_bytes = 0;
     p.mscr_bytes = 0;
     p.st_bytes = align_up(st_table_bytes(sh, p.n_groups), 256) + (size_t)p.n_groups * R * 8;
 }
@@ -890,6 +907,7 @@ void launch_k2_tiled(const pq_index_s* idx, const K2Plan& p, int B, int K,
     (void)mscr;
     K2TArgs a{};
     a.codes = idx->d_codes3;
+    a.codes_bytes = idx->v3_code_bytes;
     a.perm = idx->d_perm3;
     a.St = St;
     a.n_tiles = idx->v3_tiles;

@@ -234,9 +234,12 @@ __global__ void __launch_bounds__(K6_THREADS) k6_query(const K6Args a) {
             __threadfence();
             atomicAdd(gb, 1u);
             unsigned int seen;
+            long long spins = 0;
+            (void)spins;
             do {
                 asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(gb) : "memory");
                 if (seen < gridDim.x) __nanosleep(64);
+                PQ_SPIN_CHECK(spins);                  // checked builds: a missing CTA traps
             } while (seen < gridDim.x);
         }
         __syncthreads();
@@ -609,6 +612,7 @@ __global__ void __launch_bounds__(K6_THREADS) k6_query(const K6Args a) {
                 int base = 0;
                 if (lane == 0) base = atomicAdd(&count, __popc(bm));
                 base = __shfl_sync(FULL, base, 0);
+                PQ_DCHECK(base + __popc(bm) <= a.chunks * a.K);   // mk holds >= chunks * K keys (plan)
                 if (keep) mk[base + __popc(bm & lanemask_lt())] = v[q];
             }
         }

@@ -1,5 +1,5 @@
-// pairing.cu — host-side construction of the K2 v2 ("paired half-warps")
-// catalogue layout, done once in pq_create (outside the hot path).
+// pairing.cu — host-side colour pairing of the catalogue rows for the
+// 16-user K2 v3 layout, done once in pq_create (outside the hot path).
 //
 // 1. Per split k, 2-colour the b sub-ids, balancing the colours by how many
 //    items use each sub-id (greedy, largest first, b/2 sub-ids per colour), and

@@ -76,7 +76,7 @@ struct TopkWs {
 static TopkWs topk_ws(const pq_index_s* idx, int B, int K) {
     TopkWs w{};
     w.plan = plan_k2(idx, B, K);
-    w.lanebuf = align_up(w.plan.lanebuf_bytes, 256) + align_up(w.plan.ghist_bytes, 256) +
+    w.lanebuf = align_up(w.plan.lanebuf_bytes, 256) +
                 align_up(w.plan.mscr_bytes, 256) + align_up(w.plan.st_bytes, 256);
     w.cand = align_up(w.plan.cand_bytes, 256);
     w.k3 = align_up(k3_reduce_scratch_bytes((int64_t)w.plan.chunks * K, B, K), 256);
@@ -90,7 +90,7 @@ static void run_score_topk(pq_index_s* idx, const float* S, int B, int K, void* 
     if (!ws || ws_bytes < w.total)
         fail(PQ_ERR_WORKSPACE, "workspace too small: need " + std::to_string(w.total) + " bytes");
     Carve c(ws);
-    uint64_t* lanebuf = c.take<uint64_t>(w.lanebuf);     // lane buffers (+ v2 flush histograms)
+    uint64_t* lanebuf = c.take<uint64_t>(w.lanebuf);     // lane buffers
     uint64_t* cand = c.take<uint64_t>(w.plan.cand_bytes);
     void* k3s = c.take<char>(k3_reduce_scratch_bytes((int64_t)w.plan.chunks * K, B, K));
     char* lb = reinterpret_cast<char*>(lanebuf);
@@ -127,7 +127,7 @@ static pq_index_s subset_index(const pq_index_s* idx, int64_t nV, uint8_t* codes
     t.d_perm = const_cast<int32_t*>(V);
     t.n_rows = nV;
     t.tuning = idx->tuning;
-    if (t.tuning.variant == 2 || t.tuning.variant == 3) t.tuning.variant = 0;
+    if (t.tuning.variant == 3) t.tuning.variant = 0;
     return t;
 }
 static size_t subset_codes_bytes(const pq_index_s* idx, int64_t nV) {
@@ -152,11 +152,8 @@ static int64_t dense_lists(int64_t N, int64_t nc) {
     return lists;
 }
 
-// K2 v2 layout (pairing.cu) when the shape is supported: b = 256, m in {4, 8, 16},
-// 16 users' tables in shared memory, or all but two splits (+2 in TMEM).
-// Host-side state shared by the layout builders of one pq_create: the codes
-// on the host (copied once if the caller passed device memory) and the colour
-// pairing (built once, used by the v2 and v3 layouts).
+// Host-side state of one pq_create's layout builder: the codes on the host
+// (copied once if the caller passed device memory) and the colour pairing.
 struct CreateCtx {
     std::vector<uint8_t> hbuf;
     const uint8_t* hc = nullptr;
@@ -186,54 +183,13 @@ static const PairLayout& pairing0(CreateCtx& cx, const pq_index_s* idx, const ui
     return cx.pair0;
 }
 
-static void build_v2_layout(pq_index_s* idx, CreateCtx& cx, const uint8_t* codes_in, const uint8_t* dev_src,
-                            cudaStream_t st) {
-    const int m = idx->m, b = idx->b;
-    const size_t budget = idx->smem_optin;
-    int tm = -1;
-    if (k2_paired_supported(m, 0, b) && k2_paired_smem(m, 0, b, 8) <= budget) tm = 0;
-    else if (k2_paired_supported(m, 2, b) && k2_paired_smem(m, 2, b, 8) <= budget) tm = 2;
-    if (tm < 0) return;
-    const PairLayout& L = pairing0(cx, idx, codes_in, dev_src, st);
-    // v2 stores the last tm splits as TMEM columns (stored code + b * t) instead of row offsets
-    std::vector<uint16_t> tcodes;
-    const uint16_t* codes16 = L.codes16.data();
-    if (tm > 0) {
-        tcodes = L.codes16;
-        const int ms = m - tm;
-        for (int64_t r = 0; r < L.rows; ++r)
-            for (int k = ms; k < m; ++k) {
-                uint16_t& c = tcodes[(size_t)r * m + k];
-                c = (uint16_t)(c / 64u + (uint32_t)b * (uint32_t)(k - ms));
-            }
-        codes16 = tcodes.data();
-    }
-    const size_t cbytes = (size_t)(L.rows + V2_PAD_ROWS) * m * 2;
-    PQ_CUDA(cudaMalloc(&idx->d_codes16, cbytes));
-    PQ_CUDA(cudaMalloc(&idx->d_perm16, (size_t)L.rows * 4));
-    PQ_CUDA(cudaMalloc(&idx->d_cmap16, (size_t)m * b));
-    PQ_CUDA(cudaMalloc(&idx->d_pos16, (size_t)m * b));
-    PQ_CUDA(cudaMemcpyAsync(idx->d_pos16, L.pos.data(), (size_t)m * b, cudaMemcpyHostToDevice, st));
-    PQ_CUDA(cudaMemsetAsync(idx->d_codes16, 0, cbytes, st));
-    PQ_CUDA(cudaMemcpyAsync(idx->d_codes16, codes16, (size_t)L.rows * m * 2, cudaMemcpyHostToDevice, st));
-    PQ_CUDA(cudaMemcpyAsync(idx->d_perm16, L.perm.data(), (size_t)L.rows * 4, cudaMemcpyHostToDevice, st));
-    PQ_CUDA(cudaMemcpyAsync(idx->d_cmap16, L.cmap.data(), (size_t)m * b, cudaMemcpyHostToDevice, st));
-    PQ_CUDA(cudaStreamSynchronize(st));
-    idx->v2_ok = 1;
-    idx->v2_tm = tm;
-    idx->v2_rows = L.rows;
-    idx->v2_matched = L.matched_pairs;
-    idx->v2_leftover = L.leftover;
-}
-
 // K2 v3 layout (k2_tiled.cu).  R = 16: the colour pairing (every split in
 // shared memory); R = 32: item order; with an exact first-pair table (b = 16)
 // split 0's stored code is g0 + 16 g1 and splits 2.. follow.  Rows are padded
 // to whole tiles and the codes phase-blocked ([tile][phase][row][pss], pss >=
 // ps stored bytes per row per phase).
 static void free_index_buffers(pq_index_s* idx) {
-    void* bufs[] = {idx->d_codes, idx->d_perm, idx->d_cmap, idx->d_codes16, idx->d_perm16, idx->d_cmap16,
-                    idx->d_pos16, idx->d_codes3, idx->d_perm3, idx->d_cmap3};
+    void* bufs[] = {idx->d_codes, idx->d_perm, idx->d_cmap, idx->d_codes3, idx->d_perm3, idx->d_cmap3};
     for (void* p : bufs)
         if (p) cudaFree(p);
 }
@@ -293,6 +249,7 @@ static void build_v3_layout(pq_index_s* idx, CreateCtx& cx, const uint8_t* codes
     }
     const size_t cbytes = c3.size() + V3_CODE_PAD;
     PQ_CUDA(cudaMalloc(&idx->d_codes3, cbytes));
+    idx->v3_code_bytes = (int64_t)cbytes;
     PQ_CUDA(cudaMalloc(&idx->d_perm3, p3.size() * 4));
     PQ_CUDA(cudaMalloc(&idx->d_cmap3, (size_t)m * b));
     PQ_CUDA(cudaMemsetAsync(idx->d_codes3, 0, cbytes, st));
@@ -392,10 +349,9 @@ pq_status pq_create_ex(const uint8_t* codes, int64_t N, int32_t m, int32_t b, in
                      (long long)(bad / m), (long long)(bad % m), (unsigned)v, b);
             fail(PQ_ERR_CODE_RANGE, msg);
         }
-        need((flags & ~(PQ_CREATE_SMALL_BATCH_ONLY | PQ_CREATE_WITH_V2)) == 0, "unknown pq_create flags");
+        need((flags & ~PQ_CREATE_SMALL_BATCH_ONLY) == 0, "unknown pq_create flags");
         if (!(flags & PQ_CREATE_SMALL_BATCH_ONLY)) {
             CreateCtx cx;
-            if (flags & PQ_CREATE_WITH_V2) build_v2_layout(idx, cx, codes, src, st);
             build_v3_layout(idx, cx, codes, src, st);
         }
         if (tmp) { cudaFree(tmp); tmp = nullptr; }
@@ -441,20 +397,20 @@ pq_status pq_index_layout(pq_index idx, int32_t* paired, int32_t* tmem_splits,
                           int64_t* pairs_matched, int64_t* leftover_items) {
     PQ_API_BEGIN
     need(idx != nullptr, "index is NULL");
-    // the colour pairing is shared by the v2 and v3 layouts (pq_create); for m > 20
-    // it pairs complementary colours on the first 20 splits
+    // the colour pairing of the v3 layout (pq_create); for m > 20 it pairs
+    // complementary colours on the first 20 splits
     const bool p3 = idx->v3_ok && idx->v3_R == 16;
-    if (paired) *paired = (idx->v2_ok || p3) ? 1 : 0;
-    if (tmem_splits) *tmem_splits = idx->v2_ok ? idx->v2_tm : 0;
-    if (pairs_matched) *pairs_matched = idx->v2_ok ? idx->v2_matched : (p3 ? idx->v3_matched : 0);
-    if (leftover_items) *leftover_items = idx->v2_ok ? idx->v2_leftover : (p3 ? idx->v3_leftover : 0);
+    if (paired) *paired = p3 ? 1 : 0;
+    if (tmem_splits) *tmem_splits = 0;
+    if (pairs_matched) *pairs_matched = p3 ? idx->v3_matched : 0;
+    if (leftover_items) *leftover_items = p3 ? idx->v3_leftover : 0;
     PQ_API_END
 }
 
 pq_status pq_index_variants(pq_index idx, int32_t* mask) {
     PQ_API_BEGIN
     need(idx != nullptr && mask != nullptr, "NULL argument");
-    *mask = 2 | (idx->v2_ok ? 4 : 0) | (idx->v3_ok ? 8 : 0) | (k2_latency_supported(idx, 1, 1) ? 16 : 0);
+    *mask = 2 | (idx->v3_ok ? 8 : 0) | (k2_latency_supported(idx, 1, 1) ? 16 : 0);
     PQ_API_END
 }
 

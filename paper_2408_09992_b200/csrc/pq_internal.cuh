@@ -36,6 +36,30 @@ inline void count_launch(int n = 1) { g_launches.fetch_add(n, std::memory_order_
 #define PQ_CUDA(x) ::pq::check_cuda((x), #x)
 
 // ----------------------------------------------------------------------------
+// Checked builds (python -m paper_2408_09992_b200.build --checked ->
+// libpqtopk_checked.so, -DPQTOPK_CHECKED): device-side bounds / invariant
+// checks and bounded spin-waits (PQ_SPIN_LIMIT polls) that report the failing
+// site and trap instead of corrupting memory or hanging.  This stands in for
+// compute-sanitizer, which this GPU pool does not allow.  Product builds
+// compile every check away.
+// ----------------------------------------------------------------------------
+#ifdef PQTOPK_CHECKED
+#define PQ_DCHECK(cond)                                                                      \
+    do {                                                                                     \
+        if (!(cond)) {                                                                       \
+            printf("PQ_DCHECK failed: %s at %s:%d (block %d thread %d)\n", #cond, __FILE__,  \
+                   __LINE__, (int)blockIdx.x, (int)threadIdx.x);                             \
+            __trap();                                                                        \
+        }                                                                                    \
+    } while (0)
+constexpr long long PQ_SPIN_LIMIT = 1ll << 27;
+#define PQ_SPIN_CHECK(counter) PQ_DCHECK(++(counter) < ::pq::PQ_SPIN_LIMIT)
+#else
+#define PQ_DCHECK(cond) do { } while (0)
+#define PQ_SPIN_CHECK(counter) do { } while (0)
+#endif
+
+// ----------------------------------------------------------------------------
 // Ranking key (reading R3): 64-bit unsigned, larger = ranks earlier.
 //   high 32 bits: order-preserving image of the fp32 score bits
 //   low  32 bits: 0xFFFFFFFF - global id   (smaller id ranks earlier on ties)
@@ -63,7 +87,8 @@ struct Layout {
     int32_t paired;        // 1: rows are in pair order (see k0), d_perm valid
 };
 
-// K2 v2 catalogue layout (pairing.cu), built on the host in pq_create.
+// Colour-paired catalogue rows (pairing.cu), built on the host in pq_create
+// for the 16-user K2 v3 layout.
 struct PairLayout {
     std::vector<uint16_t> codes16;   // [rows][m]
     std::vector<int32_t> perm;       // [rows]
@@ -88,18 +113,11 @@ struct pq_index_s {
     int32_t* d_perm = nullptr;     // row -> local item id (only if lay.paired)
     uint8_t* d_cmap = nullptr;     // [m][b] stored code -> original code (paired)
     int64_t n_rows = 0;            // rows in d_codes (>= N when paired, padded)
-    // K2 v2 ("paired half-warps") layout; v2_ok = 0 when not eligible
-    int v2_ok = 0;
-    int v2_tm = 0;                 // splits served from TMEM (0 or 2)
-    int64_t v2_rows = 0, v2_matched = 0, v2_leftover = 0;
-    uint16_t* d_codes16 = nullptr; // [v2_rows + pad][m]
-    int32_t* d_perm16 = nullptr;   // [v2_rows]
-    uint8_t* d_cmap16 = nullptr;   // [m][b] stored -> original
-    uint8_t* d_pos16 = nullptr;    // [m][b] original -> stored
     // K2 v3 ("tiled phases") layout; v3_ok = 0 when not eligible
     int v3_ok = 0;
     int v3_R = 0;                  // users per table row (16: paired layout, 32: item order)
     int64_t v3_tiles = 0;          // tiles of k2_tiled_rows_per_tile(v3_R) rows
+    int64_t v3_code_bytes = 0;     // allocated bytes of d_codes3 (incl. V3_CODE_PAD)
     int64_t v3_matched = 0, v3_leftover = 0;
     void* d_codes3 = nullptr;      // [tiles][NP][TR][PS] stored codes, k2_tiled_code_bytes() each (+ pad)
     int32_t* d_perm3 = nullptr;    // [tiles * 4096] row -> local id (-1 = padding)
@@ -132,7 +150,6 @@ struct K2Plan {
     size_t smem = 0;
     size_t lanebuf_bytes = 0;     // grid * W * 32 * cap * 8
     size_t cand_bytes = 0;        // B * chunks * K * 8
-    size_t ghist_bytes = 0;       // v2: grid * W * 256 * 4
     size_t mscr_bytes = 0;        // grid * 32 * W * K * 8 (end-of-unit merge scratch)
     int variant = 1;
     int tm = 0;
@@ -173,12 +190,6 @@ void launch_k2_tiled_prep(const pq_index_s* idx, const K2Plan& p, const float* S
                           cudaStream_t st);
 void launch_k2_tiled(const pq_index_s* idx, const K2Plan& p, int B, int K,
                      uint64_t* lanebuf, uint64_t* mscr, const float* St, uint64_t* cand, cudaStream_t st);
-// v2 helpers (k2_paired.cu)
-size_t k2_paired_smem(int m, int tm, int b, int W);
-bool k2_paired_supported(int m, int tm, int b);
-int k2_paired_warps(int m, int tm, int b);
-int k2_paired_depth(int m, int tm, int b);
-constexpr int V2_PAD_ROWS = 1 << 16;     // zero rows after the last pair (unclamped loads)
 K2Plan plan_k2(const pq_index_s* idx, int B, int K);
 void launch_k2(const pq_index_s* idx, const K2Plan& p, const float* S, int B, int K,
                uint64_t* lanebuf, uint64_t* cand, cudaStream_t st);

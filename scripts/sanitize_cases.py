@@ -1,10 +1,12 @@
-"""Small cases for compute-sanitizer (memcheck / racecheck / synccheck / initcheck).
+"""Small cases for the checked build (scripts/checked_run.sh) -- the stand-in
+for compute-sanitizer, which this GPU pool does not allow.
 
-    compute-sanitizer --tool racecheck python scripts/sanitize_cases.py [case ...]
+    PQTOPK_CHECKED=1 python scripts/sanitize_cases.py [--reps R] [case ...]
 
-Every kernel family of the library runs once on a C1/C2-sized input and its
-answer is checked bit-exactly against the CPU oracle (so a sanitizer-clean run
-is also a parity run).  Cases (SURVEY.md §5 "race detection"):
+Every kernel family of the library runs R times on a C1/C2-sized input and
+each answer is checked bit-exactly against the CPU oracle (a race shows up as
+a parity failure; a bounds violation or a hang as a PQ_DCHECK trap in the
+checked library).  Cases (SURVEY.md §5 "race detection"):
   tiled16   K2 v3 m = 16 (TMA phase tables + TMEM partial sums), shrink_watermark = 1
             (forces the tile-end shrink protocol on every tile)
   tiled8    K2 v3 m = 8 single-phase tables with threshold seeding, shrink_watermark = 1
@@ -124,5 +126,13 @@ def main(cases):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1:] or ["tiled16", "tiled8", "tiled4", "latency", "k6grid", "k6clus", "merge",
-                          "subset", "recjpq", "dense"])
+    argv = sys.argv[1:]
+    reps = 1
+    if argv[:1] == ["--reps"]:
+        reps, argv = int(argv[1]), argv[2:]
+    cases = argv or ["tiled16", "tiled8", "tiled4", "latency", "k6grid", "k6clus", "merge", "subset",
+                     "recjpq", "dense"]
+    import paper_2408_09992_b200 as _pq
+    print("library:", _pq.lib_path(), flush=True)
+    for _ in range(reps):
+        main(cases)
