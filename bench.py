@@ -381,6 +381,9 @@ def run_ours(args):
     with sampler:
         barrier()
         torch.cuda.synchronize()
+        # the GPU idles ~2 ms while the host enqueues every timed step, so a host
+        # hiccup (GIL, sampler thread) can never open a gap inside a timed step
+        torch.cuda._sleep(4_000_000)
         for e0, e1 in evs:
             flush.fill_(1)
             e0.record()

@@ -52,6 +52,7 @@
 #include <climits>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <vector>
 
 #include "k2_common.cuh"
@@ -578,6 +579,7 @@ __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
                                 if (!(cmask >> (4 * d + j) & 1u) || !(vv[j] >= tf[j])) continue;
                                 const int u = 4 * q + j;
                                 const int p = atomicAdd(&cnt_u[u], 1);
+                                if (a.dbg) atomicAdd(reinterpret_cast<unsigned long long*>(a.dbg + 16), 1ull);   // diagnostics: inserts
                                 if (p >= a.cap) __trap();      // protocol invariant: cap >= wm + 3 TR
                                 ubuf[(int64_t)u * a.cap + p] = make_raw(vv[j] + 0.0f, row);
                                 if (p == wm) {
@@ -642,6 +644,7 @@ __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
                 *reinterpret_cast<volatile int*>(&sflag[(tseq - 1) & 1]) == (int)tseq);
             if (need) {                                // uniform across the CTA
                 __syncthreads();                       // every insert so far is visible
+                if (a.dbg && threadIdx.x == 0) atomicAdd(a.dbg + 18, 1);   // diagnostics: shrinks
                 for (int u = warp; u < n_valid; u += W) {
                     const int n = cnt_u[u];
                     if (n <= a.K) continue;
@@ -943,12 +946,16 @@ void launch_k2_tiled(const pq_index_s* idx, const K2Plan& p, int B, int K,
     count_launch();
     check_launch("k2_tiled");
     if (a.dbg) {
-        int h[16];
+        int h[20];
         PQ_CUDA(cudaMemcpyAsync(h, a.dbg, sizeof h, cudaMemcpyDeviceToHost, st));
         PQ_CUDA(cudaStreamSynchronize(st));
         cudaFree(a.dbg);
-        fprintf(stderr, "k2_tiled debug: stuck=%d cta=%d warp=%d tseq=%d arrivals=%d unit=%d t=%d ntl=%d sflag=%d,%d\n",
-                h[0], h[1], h[2], h[3], h[4], h[5], h[6], h[7], h[8], h[9]);
+        unsigned long long ins = 0;
+        memcpy(&ins, h + 16, 8);
+        fprintf(stderr, "k2_tiled debug: stuck=%d cta=%d warp=%d tseq=%d arrivals=%d unit=%d t=%d ntl=%d sflag=%d,%d "
+                "inserts=%llu (%.1f per user) shrinks=%d units=%lld\n",
+                h[0], h[1], h[2], h[3], h[4], h[5], h[6], h[7], h[8], h[9], ins, (double)ins / B, h[18],
+                (long long)p.n_groups * p.chunks);
     }
     if (a.trace) {                       // diagnostics only: dump CTA 0's phase timeline
         std::vector<long long> h(tn);

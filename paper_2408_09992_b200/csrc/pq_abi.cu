@@ -351,8 +351,12 @@ pq_status pq_create_ex(const uint8_t* codes, int64_t N, int32_t m, int32_t b, in
         }
         need((flags & ~PQ_CREATE_SMALL_BATCH_ONLY) == 0, "unknown pq_create flags");
         if (!(flags & PQ_CREATE_SMALL_BATCH_ONLY)) {
-            CreateCtx cx;
-            build_v3_layout(idx, cx, codes, src, st);
+            if (getenv("PQTOPK_HOST_LAYOUT")) {        // the host builder (A/B and cross-check only)
+                CreateCtx cx;
+                build_v3_layout(idx, cx, codes, src, st);
+            } else {
+                build_v3_layout_gpu(idx, st);          // k0_layout.cu
+            }
         }
         if (tmp) { cudaFree(tmp); tmp = nullptr; }
         cudaFree(d_bad);

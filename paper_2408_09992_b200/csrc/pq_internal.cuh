@@ -179,6 +179,8 @@ void launch_k2_latency(const pq_index_s* idx, const K2Plan& p, const float* S, i
 struct TiledShape { int R = 0, pair = 0, m_v = 0, ps = 0, pss = 0, bt = 0, bt0 = 0; };
 TiledShape k2_tiled_shape(int m, int b);
 size_t k2_tiled_smem(const TiledShape& t, int W);
+// the K2 v3 catalogue layout built on the GPU from d_codes (k0_layout.cu)
+void build_v3_layout_gpu(pq_index_s* idx, cudaStream_t st);
 bool k2_tiled_supported(int m, int b);
 int k2_tiled_users(int m, int b);
 int k2_tiled_code_bytes();

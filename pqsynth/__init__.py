@@ -68,6 +68,9 @@ CONFIGS = {
                  note="next row f2: m = 64 splits (Fig. 2b, PAPER.md:257), not a BASELINE config"),
     "c7": Config("c7", 7, 1_000_000_000, 8, 256, 512, 1, 10,
                  note="next row f2: 10^9 items (RQ2, PAPER.md:255), single user; not a BASELINE config"),
+    "c7b": Config("c7b", 7, 1_000_000_000, 8, 256, 512, 128, 10,
+                  note="10^9 items (RQ2, PAPER.md:255) for a BATCH of 128 users (same codes as c7): the "
+                       "batched layout built on the GPU; not a BASELINE config"),
     "c5": Config("c5", 5, 200_000_000, 4, 16, 64, 4096, 1000, gpus=(8,),
                  note="tie stress: 65,536 code tuples"),
 }

@@ -424,6 +424,9 @@ FUSED_CASES = [
     (526, 300_007, 16, 200, 128, 4, 64, "zipf"),       # b not a power of 2, ragged tail
     (527, 2_000_003, 16, 256, 64, 4, 100, "uniform"),  # many chunks per user, 8 table copies
     (528, 900_001, 8, 256, 256, 2, 50, "zipf"),        # skewed codes, d/m = 32
+    (529, 20_000_003, 8, 256, 64, 1, 10, "uniform"),   # long chunks (thousands of rounds per CTA)
+    (530, 500_001, 8, 128, 64, 2, 20, "zipf"),         # b = 128
+    (531, 3_000_001, 4, 256, 64, 3, 100, "uniform"),   # m = 4
 ]
 
 
@@ -440,7 +443,8 @@ def test_fused_query_parity(pq, torch, orc, case):
     check_S(orc, F, P, S_ref)
     ref = orc.pq_topk(G, S_ref, K, id_base=seed)
     assert idx.search_plan(B, d, K)["variant"] == 5
-    for tun in (dict(), dict(cluster=1), dict(cluster=2, chunks=6), dict(cluster=8), dict(variant=5, chunks=1)):
+    for tun in (dict(), dict(cluster=1), dict(cluster=2, chunks=6), dict(cluster=8), dict(variant=5, chunks=1),
+                dict(chunks=3), dict(users_per_row=8, chunks=4)):
         idx.set_tuning(**tun)
         S_out = torch.full((B, m, b), float("nan"), device="cuda")
         i, s = pq.pq_search(idx, Fd, Pd, K, S_out=S_out)
@@ -578,3 +582,31 @@ def test_search_plan_and_flags(pq, torch):
                         0x100, ctypes.c_void_p(ws.data_ptr()), nb, ctypes.c_void_p(ids.data_ptr()),
                         ctypes.c_void_p(sc.data_ptr()), None, None)
     assert st != 0 and b"flags" in L.pq_last_error()
+
+
+@pytest.mark.parametrize("N,m,b,dist", [(1_500_001, 16, 256, "uniform"), (150_001, 8, 256, "zipf"),
+                                        (300_001, 4, 16, "uniform"), (60_001, 64, 256, "uniform"),
+                                        (9_000, 16, 256, "few"), (3, 8, 256, "uniform")])
+def test_gpu_layout_builder(pq, torch, orc, N, m, b, dist):
+    """a0 on the GPU (k0_layout.cu): the K2 v3 layout built from the device
+    code rows has the same pairing statistics as the host builder (the counts
+    are deterministic; the order inside a class is not), and both indexes give
+    the oracle's answer bit for bit (Eq. 1; results independent of the
+    layout, R4)."""
+    G, P, F = pqsynth.random_instance(880 + m, N, m, b, 4 * m, 20, code_dist=dist)
+    S_t = pq.pq_subscores(cuda(torch, F), cuda(torch, P))
+    ref = orc.pq_topk(G, S_t.cpu().numpy(), 50, id_base=5)
+    gpu_idx = pq.pq_create(cuda(torch, G), b=b, id_base=5)    # device codes
+    os.environ["PQTOPK_HOST_LAYOUT"] = "1"
+    try:
+        host_idx = pq.pq_create(G, b=b, id_base=5)
+    finally:
+        del os.environ["PQTOPK_HOST_LAYOUT"]
+    assert gpu_idx.layout() == host_idx.layout()
+    for idx in (gpu_idx, host_idx):
+        if 3 in idx.variants():
+            assert idx.plan(20, 50)["variant"] == 3
+        i, s = pq.pq_score_topk(idx, S_t, 50)
+        assert_same(i.cpu().numpy(), s.cpu().numpy(), *ref)
+        W = pq.pq_reconstruct(idx, cuda(torch, P)).cpu().numpy()
+        assert np.array_equal(W, orc.reconstruct(G, P))
