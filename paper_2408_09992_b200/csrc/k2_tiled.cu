@@ -79,8 +79,9 @@ struct K2TArgs {
     int n_groups, chunks;
     int64_t chunk_tiles;       // tiles per item chunk
     uint64_t* ubuf;            // [grid][R][cap] per-user candidate buffers
-    int cap;                   // >= 2K + 3 TR + 96 (see the shrink protocol)
-    int wm;                    // shrink watermark (<= cap - 3 TR - 32)
+    int cap;                   // >= 2K + (2 slack + 1) TR + 96 (see the shrink protocol)
+    int wm;                    // shrink watermark (<= cap - (2 slack + 1) TR - 32)
+    int slack;                 // tiles of warp skew allowed at a tile end (1..3)
     uint64_t* cand;            // [B][chunks][K]
     unsigned long long* gtau;  // [n_groups * R] per-user proved thresholds (zeroed per call)
     long long* trace;          // diagnostics (PQTOPK_K2_TRACE): CTA 0 phase timeline, or null
@@ -273,6 +274,7 @@ __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
     static_assert(R == 16 || R == 32, "users per row");
 
     extern __shared__ __align__(1024) unsigned char sm_raw[];
+    const long long t_kstart = a.dbg ? clock64() : 0;   // diagnostics (PQTOPK_K2_DEBUG)
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     // smem: [tables NB x TBLB][hist W x 1 KB][tau R x u64][cnt R][nconv R][mbar NB][done NB][tmem]
@@ -284,8 +286,8 @@ __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
     unsigned long long* mbar = reinterpret_cast<unsigned long long*>(nconv_u + R);
     int* done = reinterpret_cast<int*>(mbar + NB);
     int* tiles_done = done + NB;                       // [W] tiles finished by each warp
-    int* sflag = tiles_done + W;                       // [2] shrink request: tile index + 1
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sflag + 2);
+    int* sflag = tiles_done + W;                       // [4] shrink requests (ring of slack + 1)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sflag + 4);
     constexpr int LM = RPS * W;                        // lanes per user in the CTA
     uint64_t* lmk = reinterpret_cast<uint64_t*>(sm_raw + align_up((size_t)(reinterpret_cast<char*>(tmem_slot + 4) -
                                                                   reinterpret_cast<char*>(sm_raw)), 16));
@@ -327,7 +329,7 @@ __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
     }
     if (threadIdx.x < R) { tau_sh[threadIdx.x] = 0ull; cnt_u[threadIdx.x] = 0; nconv_u[threadIdx.x] = 0; }
     if (threadIdx.x < W) tiles_done[threadIdx.x] = 0;
-    if (threadIdx.x == 0) { sflag[0] = 0; sflag[1] = 0; }
+    if (threadIdx.x < 4) sflag[threadIdx.x] = 0;
     uint32_t tmem_base = 0;
     if constexpr (NP > 1) {
         if (warp == 0) {
@@ -367,14 +369,17 @@ __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
     uint64_t* ubuf = a.ubuf + (int64_t)blockIdx.x * R * a.cap;
     int64_t gseq = 0;                                  // table uses so far (NP > 1)
     int64_t useq = 0;                                  // units done by this CTA (NP == 1)
-    // Shrink protocol (no per-tile barrier): the insert that takes a user's
-    // buffer to `wm` entries during tile T records T + 1 in sflag[T & 1]; at
-    // the end of tile T + 1 every warp (having waited until all warps finished
-    // tile T) sees the same flag and the CTA shrinks.  Warps drift by up to one
-    // tile (a warp passes the end of tile T once all warps finished T - 1), so
-    // when a warp in tile T makes the request, slower warps may still insert
-    // the rest of tile T - 1; with tiles T and T + 1 that is at most 3 * TR
-    // entries per user before the shrink: cap >= wm + 3 * TR.
+    // Shrink protocol (no per-tile barrier), with a skew allowance of S = slack
+    // tiles: the insert that takes a user's buffer to `wm` entries during tile
+    // T records T + S in sflag[T % (S + 1)]; at the end of tile T + S every warp
+    // (having waited until all warps finished tile T) sees the same flag and the
+    // CTA shrinks (a warp passes the end of tile X once all warps finished X - S).
+    // Uniformity: a warp reads the slot only after every warp finished tile T,
+    // so the flag is final; a request forces a CTA barrier before anyone can
+    // start tile T + S + 1, whose requests reuse the slot.  Capacity: when a warp
+    // in tile T makes the request, slower warps may still be in tile T - S; with
+    // tiles up to T + S that is at most (2S + 1) * TR entries per user before
+    // the shrink: cap >= wm + (2S + 1) * TR.
     const int wm = a.wm;
     int64_t tseq = 0;                                  // tiles done by this CTA
 
@@ -580,10 +585,11 @@ __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
                                 const int u = 4 * q + j;
                                 const int p = atomicAdd(&cnt_u[u], 1);
                                 if (a.dbg) atomicAdd(reinterpret_cast<unsigned long long*>(a.dbg + 16), 1ull);   // diagnostics: inserts
-                                if (p >= a.cap) __trap();      // protocol invariant: cap >= wm + 3 TR
+                                if (p >= a.cap) __trap();      // protocol invariant: cap >= wm + (2S + 1) TR
                                 ubuf[(int64_t)u * a.cap + p] = make_raw(vv[j] + 0.0f, row);
                                 if (p == wm) {
-                                    *reinterpret_cast<volatile int*>(&sflag[tseq & 1]) = (int)(tseq + 1);
+                                    *reinterpret_cast<volatile int*>(&sflag[(uint32_t)tseq % (uint32_t)(a.slack + 1)]) =
+                                        (int)(tseq + a.slack);
                                     __threadfence_block();
                                 }
                             }
@@ -620,12 +626,15 @@ __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
             // outstanding global loads; the only cross-warp data read without a
             // barrier is sflag, fenced by its writer, and __syncwarp orders the
             // writer lane before lane 0's tiles_done store)
+            const long long t_eot = a.dbg ? clock64() : 0;   // diagnostics (PQTOPK_K2_DEBUG)
             __syncwarp();
             if (lane == 0) *reinterpret_cast<volatile int*>(&tiles_done[warp]) = (int)(tseq + 1);
-            // wait until every warp has finished tile T - 1 (bounds the skew to one tile)
+            // wait until every warp has finished tile T - S (bounds the skew to S tiles)
             for (long long spins = 0;; ++spins) {
+                if (a.dbg && spins == 1 && lane == 0)
+                    atomicAdd(reinterpret_cast<unsigned long long*>(a.dbg + 24), 1ull);   // waits
                 const int td = lane < W ? *reinterpret_cast<volatile int*>(&tiles_done[lane]) : INT_MAX;
-                if (__all_sync(FULL, td >= (int)tseq)) break;
+                if (__all_sync(FULL, td >= (int)tseq - a.slack + 1)) break;
                 PQ_DCHECK(spins < PQ_SPIN_LIMIT);      // checked builds: a lost warp traps
                 __nanosleep(64);                       // back off: spinning would steal smem cycles
                 if (a.dbg && spins > (1ll << 26)) {
@@ -640,8 +649,10 @@ __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
             // (always after a unit's first tile: it ran with the unit's initial,
             // usually weak or only seeded, thresholds -- an early exact K-th keeps
             // the next tiles' candidate lists short; measured: C3 -1.1%)
-            const bool need = (t == 0) || (tseq > 0 &&
-                *reinterpret_cast<volatile int*>(&sflag[(tseq - 1) & 1]) == (int)tseq);
+            const bool need = (t == 0) || (tseq >= a.slack &&
+                *reinterpret_cast<volatile int*>(&sflag[(uint32_t)(tseq - a.slack) % (uint32_t)(a.slack + 1)]) ==
+                    (int)tseq);
+            const long long t_shr = a.dbg ? clock64() : 0;
             if (need) {                                // uniform across the CTA
                 __syncthreads();                       // every insert so far is visible
                 if (a.dbg && threadIdx.x == 0) atomicAdd(a.dbg + 18, 1);   // diagnostics: shrinks
@@ -668,6 +679,11 @@ __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
 #pragma unroll
                 for (int j = 0; j < 4; ++j)
                     if (tf[j] != INFINITY) tf[j] = fmaxf(tf[j], tau_to_filter(tau_sh[4 * q + j]));
+            }
+            if (a.dbg && lane == 0) {
+                const long long t_end = clock64();
+                atomicAdd(reinterpret_cast<unsigned long long*>(a.dbg + 20), (unsigned long long)(t_end - t_eot));
+                atomicAdd(reinterpret_cast<unsigned long long*>(a.dbg + 22), (unsigned long long)(t_end - t_shr));
             }
             ++tseq;
         }
@@ -702,6 +718,10 @@ __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
         c[0] = (long long)t_start_ns; c[1] = (long long)t_end_ns; c[2] = tseq;
     }
 
+    if (a.dbg && lane == 0) {                          // diagnostics: warp lifetime
+        long long t_now = clock64();
+        atomicAdd(reinterpret_cast<unsigned long long*>(a.dbg + 26), (unsigned long long)(t_now - t_kstart));
+    }
     if constexpr (NP > 1) {
         tm_fence_before();
         __syncthreads();
@@ -823,9 +843,18 @@ size_t k2_tiled_smem(const TiledShape& t, int W) {
     const int nb = (t.m_v / t.ps) > 1 ? 3 : 1;
     const size_t tbl = (size_t)(t.bt0 + (t.ps - 1) * t.bt) * R * 4;
     const size_t base = (size_t)nb * tbl + (size_t)W * 1024 + (size_t)R * 8 + (size_t)R * 8 +
-                        3 * 8 + 3 * 4 + (size_t)(W + 2) * 4 + 16;
+                        3 * 8 + 3 * 4 + (size_t)(W + 4) * 4 + 16;
     const size_t lm = nb == 1 ? (size_t)R * (32 / (R / 4)) * W * 8 : 0;   // threshold seeding keys
     return align_up(base, 16) + lm + 16;
+}
+// Warp skew (in tiles) the tile-end protocol allows; PQTOPK_K2_SLACK = 1..3 for A/B.
+static int k2_slack() {
+    static const int s = [] {
+        const char* e = getenv("PQTOPK_K2_SLACK");
+        const int v = e ? atoi(e) : 1;
+        return v < 1 ? 1 : (v > 3 ? 3 : v);
+    }();
+    return s;
 }
 static size_t st_table_bytes(const TiledShape& t, int n_groups) {
     return (size_t)n_groups * (t.bt0 + (t.m_v - 1) * t.bt) * t.R * 4;
@@ -860,7 +889,7 @@ void plan_k2_tiled(const pq_index_s* idx, int B, int K, K2Plan& p) {
     p.tm = (sh.m_v / sh.ps) > 1 ? sh.m_v - sh.ps : 0;
     p.n_groups = (int)ceil_div(B, R);
     const int TR = k2_tiled_rows_per_tile(R);
-    p.cap = (int)align_up((size_t)(2 * K + 3 * TR + 96), 32);
+    p.cap = (int)align_up((size_t)(2 * K + (2 * k2_slack() + 1) * TR + 96), 32);
     p.smem = k2_tiled_smem(sh, p.W);
     K2TFn fn = tiled_fn_shape(sh, p.W);
     if (!fn) fail(PQ_ERR_UNSUPPORTED, "tiled scoring kernel: unsupported shape");
@@ -918,9 +947,10 @@ void launch_k2_tiled(const pq_index_s* idx, const K2Plan& p, int B, int K,
     a.id_base = (uint32_t)idx->id_base;
     a.n_groups = p.n_groups; a.chunks = p.chunks; a.chunk_tiles = p.chunk_items;
     a.ubuf = lanebuf; a.cap = p.cap; a.cand = cand;
+    a.slack = k2_slack();
     {
         const int TR = k2_tiled_rows_per_tile(p.G);
-        const int wmax = p.cap - 3 * TR - 32;
+        const int wmax = p.cap - (2 * k2_slack() + 1) * TR - 32;
         const int tw = idx->tuning.shrink_watermark;
         a.wm = tw > 0 ? std::min(std::max(tw, K + 1), wmax) : wmax;
     }
@@ -946,12 +976,19 @@ void launch_k2_tiled(const pq_index_s* idx, const K2Plan& p, int B, int K,
     count_launch();
     check_launch("k2_tiled");
     if (a.dbg) {
-        int h[20];
+        int h[28];
         PQ_CUDA(cudaMemcpyAsync(h, a.dbg, sizeof h, cudaMemcpyDeviceToHost, st));
         PQ_CUDA(cudaStreamSynchronize(st));
         cudaFree(a.dbg);
-        unsigned long long ins = 0;
+        unsigned long long ins = 0, eot = 0, shr = 0, waits = 0, life = 0;
         memcpy(&ins, h + 16, 8);
+        memcpy(&eot, h + 20, 8);
+        memcpy(&shr, h + 22, 8);
+        memcpy(&waits, h + 24, 8);
+        memcpy(&life, h + 26, 8);
+        fprintf(stderr, "k2_tiled debug: warp-cycles end-of-tile %.4f of warp lifetime (shrink part %.4f), "
+                "tile-end waits %llu\n", (double)eot / (double)(life ? life : 1), (double)shr / (double)(life ? life : 1),
+                waits);
         fprintf(stderr, "k2_tiled debug: stuck=%d cta=%d warp=%d tseq=%d arrivals=%d unit=%d t=%d ntl=%d sflag=%d,%d "
                 "inserts=%llu (%.1f per user) shrinks=%d units=%lld\n",
                 h[0], h[1], h[2], h[3], h[4], h[5], h[6], h[7], h[8], h[9], ins, (double)ins / B, h[18],
