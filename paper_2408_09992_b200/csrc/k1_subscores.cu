@@ -18,19 +18,25 @@
 //
 // Grid: (m, ceil(B/UB), ceil(b/gchunk)); a block stages psi_k (gchunk x TT tile,
 // padded rows) and phi_k for UB users in shared memory and produces the UB x
-// gchunk outputs (gchunk = b, halved while the grid is short of two waves).
+// gchunk outputs (UB x gchunk <= 2048: up to 8 per thread).  UB = 32 users per
+// block for batches (each staged psi tile then serves 32 users instead of 4:
+// C2 K1 18 -> see DESIGN.md), fewer for small B; gchunk is halved while the
+// grid is short of two waves.
+#include <cstdlib>
+
 #include "pq_internal.cuh"
 
 namespace pq {
 
-constexpr int K1_UB = 4;      // users per block
 constexpr int K1_TT = 32;     // t-tile (columns of psi_k staged per pass)
+constexpr int K1_MAXOUT = 2048;   // outputs per block (UB x gchunk)
 constexpr int K1_THREADS = 256;
 constexpr int K1_PS = K1_TT + 1;   // padded row (doubles): 2 wavefronts per 64-bit warp load
 
 // psi_k and phi_k tiles are staged in shared memory already converted to fp64
 // (each float is converted once per block, not once per use), so the inner
 // loop is fp64 fma on shared-memory operands only.
+template <int K1_UB>
 __global__ void __launch_bounds__(K1_THREADS)
 k1_subscores(const float* __restrict__ phi, const float* __restrict__ psi, int B, int d,
              int m, int b, float* __restrict__ S, int gchunk) {
@@ -44,7 +50,7 @@ k1_subscores(const float* __restrict__ phi, const float* __restrict__ psi, int B
     const int g0 = blockIdx.z * gchunk;             // sub-ids [g0, g0 + nb) of split k
     const int nb = min(gchunk, b - g0);
     const int nout = nu * nb;
-    constexpr int PER = (K1_UB * 256 + K1_THREADS - 1) / K1_THREADS;   // <= 4
+    constexpr int PER = K1_MAXOUT / K1_THREADS;       // outputs per thread (nout <= 2048)
     double acc[PER][4];
 #pragma unroll
     for (int j = 0; j < PER; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.0;
@@ -121,25 +127,35 @@ k1_subscores(const float* __restrict__ phi, const float* __restrict__ psi, int B
     }
 }
 
+template <int UB>
+static void launch_k1(const float* phi, const float* psi, int B, int d, int m, int b, float* S,
+                      cudaStream_t st) {
+    // split the sub-ids over blocks while the grid is short of two waves
+    int gchunk = std::min(b, K1_MAXOUT / UB);
+    while (gchunk > 32 && (int64_t)m * ceil_div(B, UB) * ceil_div(b, gchunk) < 2 * 148) gchunk = (gchunk + 1) / 2;
+    const size_t smem = ((size_t)gchunk * K1_PS + UB * K1_TT) * sizeof(double);
+    // gchunk <= 256: at most 256 * 33 * 8 + 32 * 32 * 8 = 75.8 KB (once per device and kernel)
+    ensure_max_smem(reinterpret_cast<const void*>(k1_subscores<UB>),
+                    (int)((std::min(256, K1_MAXOUT / UB) * K1_PS + UB * K1_TT) * sizeof(double)));
+    dim3 grid(m, (unsigned)ceil_div(B, UB), (unsigned)ceil_div(b, gchunk));
+    k1_subscores<UB><<<grid, K1_THREADS, smem, st>>>(phi, psi, B, d, m, b, S, gchunk);
+    count_launch();
+    check_launch("k1_subscores");
+}
+
 void launch_subscores(const float* phi, const float* psi, int B, int d, int m, int b,
                       float* S, cudaStream_t st) {
     if (B <= 0) return;
-    // split the sub-ids over blocks while the grid is short of two waves
-    int gchunk = b;
-    while (gchunk > 32 && (int64_t)m * ceil_div(B, K1_UB) * ceil_div(b, gchunk) < 2 * 148) gchunk = (gchunk + 1) / 2;
-    const size_t smem = ((size_t)gchunk * K1_PS + K1_UB * K1_TT) * sizeof(double);
-    static std::atomic<uint64_t> attr_set{0};       // per device (bit = ordinal)
-    int dev = 0;
-    PQ_CUDA(cudaGetDevice(&dev));
-    if (dev >= 64 || !(attr_set.load() >> dev & 1)) {   // gchunk <= 256: at most 68.6 KB
-        PQ_CUDA(cudaFuncSetAttribute(k1_subscores, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)((256 * K1_PS + K1_UB * K1_TT) * sizeof(double))));
-        if (dev < 64) attr_set.fetch_or(1ull << dev);
+    // users per block: 32 for batches (a staged psi tile serves 32 users), fewer
+    // for small B; PQTOPK_K1_UB forces one (diagnostics A/B)
+    static const int forced = [] { const char* e = getenv("PQTOPK_K1_UB"); return e ? atoi(e) : 0; }();
+    const int ub = forced ? forced : (B >= 32 ? 32 : B >= 16 ? 16 : B >= 8 ? 8 : 4);
+    switch (ub) {
+        case 32: launch_k1<32>(phi, psi, B, d, m, b, S, st); break;
+        case 16: launch_k1<16>(phi, psi, B, d, m, b, S, st); break;
+        case 8: launch_k1<8>(phi, psi, B, d, m, b, S, st); break;
+        default: launch_k1<4>(phi, psi, B, d, m, b, S, st); break;
     }
-    dim3 grid(m, (unsigned)ceil_div(B, K1_UB), (unsigned)ceil_div(b, gchunk));
-    k1_subscores<<<grid, K1_THREADS, smem, st>>>(phi, psi, B, d, m, b, S, gchunk);
-    count_launch();
-    check_launch("k1_subscores");
 }
 
 }  // namespace pq

@@ -63,6 +63,11 @@ namespace pq {
 // Stored code width: 1 = the (colour-renumbered) sub-id byte, the kernel forms
 // the row offset (code * R * 4 | quad offset) with two integer ops; 2 = 16-bit
 // pre-shifted row offsets (one op, twice the code bytes).
+// Tiles of warp skew the tile-end protocol allows (S, 1..3; -DK2_SLACK=S for
+// A/B: S = 2 / 3 measured within +-2% of S = 1 on C2-C5, r02 slack A/B).
+#ifndef K2_SLACK
+#define K2_SLACK 1
+#endif
 #ifndef K2_CODE_BYTES
 #define K2_CODE_BYTES 1
 #endif
@@ -81,7 +86,6 @@ struct K2TArgs {
     uint64_t* ubuf;            // [grid][R][cap] per-user candidate buffers
     int cap;                   // >= 2K + (2 slack + 1) TR + 96 (see the shrink protocol)
     int wm;                    // shrink watermark (<= cap - (2 slack + 1) TR - 32)
-    int slack;                 // tiles of warp skew allowed at a tile end (1..3)
     uint64_t* cand;            // [B][chunks][K]
     unsigned long long* gtau;  // [n_groups * R] per-user proved thresholds (zeroed per call)
     long long* trace;          // diagnostics (PQTOPK_K2_TRACE): CTA 0 phase timeline, or null
@@ -187,13 +191,96 @@ __device__ __forceinline__ uint64_t make_raw(float s, uint32_t row) {
     return ((uint64_t)o << 32) | row;
 }
 
+// The K-th largest of up to 32 * SR keys held in registers (key index
+// u * 32 + lane in v[u]; 0 = empty), n >= K >= 1: MSD radix select, 8 bits per
+// pass, with the early exit of warp_kth (select_dev.cuh) -- the keys are read
+// from registers, not re-read from memory on every pass.
+template <int SR>
+__device__ __forceinline__ uint64_t warp_kth_regs(const uint64_t (&v)[SR], int n, uint32_t K, uint32_t* hist) {
+    uint64_t prefix = 0;
+    uint32_t krem = K;
+    const int lane = threadIdx.x & 31;
+    for (int shift = 56; shift >= 0; shift -= 8) {
+        const uint64_t hmask = (shift == 56) ? 0ull : (~0ull << (shift + 8));
+#pragma unroll
+        for (int i = lane; i < 256; i += 32) hist[i] = 0;
+        __syncwarp();
+#pragma unroll
+        for (int u = 0; u < SR; ++u) {
+            const bool ok = (u * 32 + lane < n) && ((v[u] & hmask) == prefix);
+            hist_add(hist, ok, (uint32_t)(v[u] >> shift) & 255u);
+        }
+        __syncwarp();
+        uint32_t dg, ab;
+        warp_find_digit(hist, krem, dg, ab);
+        const uint32_t inbin = hist[dg];
+        prefix |= (uint64_t)dg << shift;
+        krem -= ab;
+        __syncwarp();
+        if (shift > 0 && inbin == krem) {              // the K-th key = the smallest key carrying prefix
+            const uint64_t pmask = ~0ull << shift;
+            uint64_t mn = ~0ull;
+#pragma unroll
+            for (int u = 0; u < SR; ++u)
+                if (u * 32 + lane < n && (v[u] & pmask) == prefix && v[u] < mn) mn = v[u];
+#pragma unroll
+            for (int o = 16; o; o >>= 1) {
+                const uint64_t t = __shfl_xor_sync(FULL, mn, o);
+                mn = t < mn ? t : mn;
+            }
+            return mn;
+        }
+    }
+    return prefix;
+}
+
 // Whole warp, one user: convert the raw tail, then keep only keys >= the K-th
 // best (and >= `floor`), writing them to `dst` (may alias ub).  Returns the
 // K-th key (0 if the buffer has fewer than K non-zero keys) and the count.
+// Buffers of up to 256 entries (a shrink at the watermark 2K + 64 for K <= 96,
+// e.g. C2's K = 10) are selected in registers: one read of the buffer instead
+// of one per radix pass (a larger register window spills in the caller).
 __device__ __noinline__ uint64_t shrink_user(uint64_t* ub, int nc, int n, int K, uint64_t floor,
                                              uint64_t* dst, uint32_t* hist, const int32_t* perm,
                                              uint32_t id_base, int& n_out) {
     const int lane = threadIdx.x & 31;
+    auto to_key = [&](uint64_t raw, int32_t lid) -> uint64_t {
+        return lid < 0 ? 0ull
+                       : ((raw & 0xFFFFFFFF00000000ull) | (uint64_t)(0xFFFFFFFFu - (id_base + (uint32_t)lid)));
+    };
+    constexpr int SR = 8;
+    if (n <= 32 * SR) {
+        uint64_t v[SR];
+#pragma unroll
+        for (int u = 0; u < SR; ++u) {
+            const int i = u * 32 + lane;
+            v[u] = i < n ? ub[i] : 0ull;
+        }
+        int32_t lid[SR];
+#pragma unroll
+        for (int u = 0; u < SR; ++u) {
+            const int i = u * 32 + lane;
+            lid[u] = (i >= nc && i < n) ? __ldg(&perm[(uint32_t)v[u]]) : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < SR; ++u) {
+            const int i = u * 32 + lane;
+            if (i >= nc && i < n) v[u] = to_key(v[u], lid[u]);
+        }
+        const uint64_t kth = n > K ? warp_kth_regs<SR>(v, n, (uint32_t)K, hist) : 0ull;
+        uint64_t th = kth > floor ? kth : floor;
+        if (th == 0ull) th = 1ull;                               // key 0 = padding: never kept
+        int pos = 0;
+#pragma unroll
+        for (int u = 0; u < SR; ++u) {
+            const bool keep = u * 32 + lane < n && v[u] >= th;
+            const unsigned bm = __ballot_sync(FULL, keep);
+            if (keep) dst[pos + __popc(bm & lanemask_lt())] = v[u];
+            pos += __popc(bm);
+        }
+        n_out = pos;
+        return kth;
+    }
     constexpr int U = 8;                               // independent loads in flight per lane
     for (int i0 = nc; i0 < n; i0 += 32 * U) {
         uint64_t r[U];
@@ -211,10 +298,7 @@ __device__ __noinline__ uint64_t shrink_user(uint64_t* ub, int nc, int n, int K,
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const int i = i0 + u * 32 + lane;
-            if (i < n)
-                ub[i] = lid[u] < 0 ? 0ull
-                                   : ((r[u] & 0xFFFFFFFF00000000ull) |
-                                      (uint64_t)(0xFFFFFFFFu - (id_base + (uint32_t)lid[u])));
+            if (i < n) ub[i] = to_key(r[u], lid[u]);
         }
     }
     __syncwarp();
@@ -274,7 +358,7 @@ __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
     static_assert(R == 16 || R == 32, "users per row");
 
     extern __shared__ __align__(1024) unsigned char sm_raw[];
-    const long long t_kstart = a.dbg ? clock64() : 0;   // diagnostics (PQTOPK_K2_DEBUG)
+    const long long t_kstart = kTrace ? clock64() : 0;  // diagnostics builds (-DK2_TRACE) only
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     // smem: [tables NB x TBLB][hist W x 1 KB][tau R x u64][cnt R][nconv R][mbar NB][done NB][tmem]
@@ -584,12 +668,12 @@ __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
                                 if (!(cmask >> (4 * d + j) & 1u) || !(vv[j] >= tf[j])) continue;
                                 const int u = 4 * q + j;
                                 const int p = atomicAdd(&cnt_u[u], 1);
-                                if (a.dbg) atomicAdd(reinterpret_cast<unsigned long long*>(a.dbg + 16), 1ull);   // diagnostics: inserts
+                                if (kTrace && a.dbg) atomicAdd(reinterpret_cast<unsigned long long*>(a.dbg + 16), 1ull);   // inserts
                                 if (p >= a.cap) __trap();      // protocol invariant: cap >= wm + (2S + 1) TR
                                 ubuf[(int64_t)u * a.cap + p] = make_raw(vv[j] + 0.0f, row);
                                 if (p == wm) {
-                                    *reinterpret_cast<volatile int*>(&sflag[(uint32_t)tseq % (uint32_t)(a.slack + 1)]) =
-                                        (int)(tseq + a.slack);
+                                    *reinterpret_cast<volatile int*>(&sflag[(uint32_t)tseq % (uint32_t)(K2_SLACK + 1)]) =
+                                        (int)(tseq + K2_SLACK);
                                     __threadfence_block();
                                 }
                             }
@@ -626,15 +710,15 @@ __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
             // outstanding global loads; the only cross-warp data read without a
             // barrier is sflag, fenced by its writer, and __syncwarp orders the
             // writer lane before lane 0's tiles_done store)
-            const long long t_eot = a.dbg ? clock64() : 0;   // diagnostics (PQTOPK_K2_DEBUG)
+            const long long t_eot = kTrace ? clock64() : 0;   // diagnostics builds only
             __syncwarp();
             if (lane == 0) *reinterpret_cast<volatile int*>(&tiles_done[warp]) = (int)(tseq + 1);
             // wait until every warp has finished tile T - S (bounds the skew to S tiles)
             for (long long spins = 0;; ++spins) {
-                if (a.dbg && spins == 1 && lane == 0)
+                if (kTrace && a.dbg && spins == 1 && lane == 0)
                     atomicAdd(reinterpret_cast<unsigned long long*>(a.dbg + 24), 1ull);   // waits
                 const int td = lane < W ? *reinterpret_cast<volatile int*>(&tiles_done[lane]) : INT_MAX;
-                if (__all_sync(FULL, td >= (int)tseq - a.slack + 1)) break;
+                if (__all_sync(FULL, td >= (int)tseq - K2_SLACK + 1)) break;
                 PQ_DCHECK(spins < PQ_SPIN_LIMIT);      // checked builds: a lost warp traps
                 __nanosleep(64);                       // back off: spinning would steal smem cycles
                 if (a.dbg && spins > (1ll << 26)) {
@@ -649,13 +733,13 @@ __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
             // (always after a unit's first tile: it ran with the unit's initial,
             // usually weak or only seeded, thresholds -- an early exact K-th keeps
             // the next tiles' candidate lists short; measured: C3 -1.1%)
-            const bool need = (t == 0) || (tseq >= a.slack &&
-                *reinterpret_cast<volatile int*>(&sflag[(uint32_t)(tseq - a.slack) % (uint32_t)(a.slack + 1)]) ==
+            const bool need = (t == 0) || (tseq >= K2_SLACK &&
+                *reinterpret_cast<volatile int*>(&sflag[(uint32_t)(tseq - K2_SLACK) % (uint32_t)(K2_SLACK + 1)]) ==
                     (int)tseq);
-            const long long t_shr = a.dbg ? clock64() : 0;
+            const long long t_shr = kTrace ? clock64() : 0;
             if (need) {                                // uniform across the CTA
                 __syncthreads();                       // every insert so far is visible
-                if (a.dbg && threadIdx.x == 0) atomicAdd(a.dbg + 18, 1);   // diagnostics: shrinks
+                if (kTrace && a.dbg && threadIdx.x == 0) atomicAdd(a.dbg + 18, 1);   // shrinks
                 for (int u = warp; u < n_valid; u += W) {
                     const int n = cnt_u[u];
                     if (n <= a.K) continue;
@@ -680,7 +764,7 @@ __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
                 for (int j = 0; j < 4; ++j)
                     if (tf[j] != INFINITY) tf[j] = fmaxf(tf[j], tau_to_filter(tau_sh[4 * q + j]));
             }
-            if (a.dbg && lane == 0) {
+            if (kTrace && a.dbg && lane == 0) {
                 const long long t_end = clock64();
                 atomicAdd(reinterpret_cast<unsigned long long*>(a.dbg + 20), (unsigned long long)(t_end - t_eot));
                 atomicAdd(reinterpret_cast<unsigned long long*>(a.dbg + 22), (unsigned long long)(t_end - t_shr));
@@ -718,7 +802,7 @@ __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
         c[0] = (long long)t_start_ns; c[1] = (long long)t_end_ns; c[2] = tseq;
     }
 
-    if (a.dbg && lane == 0) {                          // diagnostics: warp lifetime
+    if (kTrace && a.dbg && lane == 0) {                // diagnostics: warp lifetime
         long long t_now = clock64();
         atomicAdd(reinterpret_cast<unsigned long long*>(a.dbg + 26), (unsigned long long)(t_now - t_kstart));
     }
@@ -847,15 +931,7 @@ size_t k2_tiled_smem(const TiledShape& t, int W) {
     const size_t lm = nb == 1 ? (size_t)R * (32 / (R / 4)) * W * 8 : 0;   // threshold seeding keys
     return align_up(base, 16) + lm + 16;
 }
-// Warp skew (in tiles) the tile-end protocol allows; PQTOPK_K2_SLACK = 1..3 for A/B.
-static int k2_slack() {
-    static const int s = [] {
-        const char* e = getenv("PQTOPK_K2_SLACK");
-        const int v = e ? atoi(e) : 1;
-        return v < 1 ? 1 : (v > 3 ? 3 : v);
-    }();
-    return s;
-}
+static int k2_slack() { return K2_SLACK; }
 static size_t st_table_bytes(const TiledShape& t, int n_groups) {
     return (size_t)n_groups * (t.bt0 + (t.m_v - 1) * t.bt) * t.R * 4;
 }
@@ -947,7 +1023,6 @@ void launch_k2_tiled(const pq_index_s* idx, const K2Plan& p, int B, int K,
     a.id_base = (uint32_t)idx->id_base;
     a.n_groups = p.n_groups; a.chunks = p.chunks; a.chunk_tiles = p.chunk_items;
     a.ubuf = lanebuf; a.cap = p.cap; a.cand = cand;
-    a.slack = k2_slack();
     {
         const int TR = k2_tiled_rows_per_tile(p.G);
         const int wmax = p.cap - (2 * k2_slack() + 1) * TR - 32;

@@ -1,4 +1,5 @@
-"""K2 v3 candidate-insert counts for a config (PQTOPK_K2_DEBUG diagnostics):
+"""K2 v3 candidate-insert counts and end-of-tile accounting for a config (PQTOPK_K2_DEBUG
+diagnostics; the counters exist only in -DK2_TRACE builds):
     python scripts/k2_inserts.py c5"""
 import os
 import sys
