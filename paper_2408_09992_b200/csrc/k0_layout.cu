@@ -14,18 +14,22 @@
 //   1. k0_hist      per-split sub-id histograms               (GPU)
 //   2. colouring    greedy, b sub-ids per split              (host, m x 256)
 //   3. k0_sig       signatures                                (GPU)
-//   4. k0_rank      class c = min(s, ~s), side = s > ~s; rank of the item
-//                   inside (class, side) by an atomic ticket  (GPU)
-//   5. pair offsets exclusive scan of min(n0, n1) per class  (host, 2^19 classes)
-//   6. k0_emit      matched items -> rows; the rest -> leftover list (GPU)
+//   4. k0_classkey  key = 2 * class + side with class c = min(s, ~s), side = s > ~s;
+//                   a stable radix sort of the item ids by key (CUB, one-time
+//                   build step) puts each (class, side) group in id order (GPU)
+//   5. pair offsets exclusive scans of the group sizes and of min(n0, n1) per
+//                   class                                      (host, 2^19 classes)
+//   6. k0_emit      the j-th items of a class's two sides -> rows 2p, 2p+1;
+//                   the rest -> leftover list, in sorted order (GPU)
 //   7. leftovers    sorted by (signature, id); pairs whose signatures differ
 //                   from a complement in one split, then the rest in order
 //                   (host; ~2% of the items at C4)
 //   8. k0_v3_codes  stored codes -> [tile][phase][slot pair][row][2][pss] (GPU)
 //   9. k0_check     every item on exactly one row              (GPU)
-// The atomic tickets make the order of items inside a class run-dependent;
-// the scores and the top-K are not (keys are unique, R3/R4), only which items
-// share a row.
+// The layout is deterministic (and equal to the round-1 host builder's for the
+// exact pairs); the scores and the top-K never depend on it (R3/R4).
+#include <cub/device/device_radix_sort.cuh>
+
 #include <algorithm>
 #include <cstring>
 #include <numeric>
@@ -66,26 +70,30 @@ __global__ void k0_sig(const uint8_t* __restrict__ codes, int64_t N, int mp, int
     }
 }
 
-__global__ void k0_rank(const uint32_t* __restrict__ sig, int64_t N, uint32_t mask, uint32_t ncls,
-                        unsigned int* __restrict__ cnt, uint32_t* __restrict__ rank) {
+// sort key 2 * class + side (and the item id as the value), group sizes
+__global__ void k0_classkey(const uint32_t* __restrict__ sig, int64_t N, uint32_t mask,
+                            uint32_t* __restrict__ key, int32_t* __restrict__ val, unsigned int* __restrict__ cnt) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x) {
         const uint32_t s = sig[i], c = s ^ mask;
-        const uint32_t cls = s < c ? s : c, side = s < c ? 0u : 1u;
-        rank[i] = atomicAdd(&cnt[side * ncls + cls], 1u);
+        const uint32_t k = 2u * (s < c ? s : c) + (s < c ? 0u : 1u);
+        key[i] = k;
+        val[i] = (int32_t)i;
+        atomicAdd(&cnt[k], 1u);
     }
 }
 
-__global__ void k0_emit(const uint32_t* __restrict__ sig, const uint32_t* __restrict__ rank, int64_t N,
-                        uint32_t mask, uint32_t ncls, const unsigned int* __restrict__ cnt,
-                        const unsigned int* __restrict__ off, int32_t* __restrict__ rowitem,
-                        int32_t* __restrict__ left, unsigned int* __restrict__ nleft) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x) {
-        const uint32_t s = sig[i], c = s ^ mask;
-        const uint32_t cls = s < c ? s : c, side = s < c ? 0u : 1u;
-        const uint32_t npc = min(cnt[cls], cnt[ncls + cls]);
-        const uint32_t r = rank[i];
-        if (r < npc) rowitem[2 * ((int64_t)off[cls] + r) + side] = (int32_t)i;
-        else left[atomicAdd(nleft, 1u)] = (int32_t)i;
+// sorted position p (item val[p] of group key[p], rank p - gstart[key]): the
+// first min(n0, n1) items of each side of a class are paired in order
+__global__ void k0_emit(const uint32_t* __restrict__ key, const int32_t* __restrict__ val, int64_t N,
+                        const unsigned int* __restrict__ cnt, const int64_t* __restrict__ gstart,
+                        const int64_t* __restrict__ poff, const int64_t* __restrict__ loff,
+                        int32_t* __restrict__ rowitem, int32_t* __restrict__ left) {
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < N; p += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t k = key[p], cls = k >> 1, side = k & 1u;
+        const uint32_t npc = min(cnt[2 * cls], cnt[2 * cls + 1]);
+        const int64_t r = p - gstart[k];
+        if (r < (int64_t)npc) rowitem[2 * (poff[cls] + r) + side] = val[p];
+        else left[loff[k] + (r - npc)] = val[p];      // leftovers in sorted (class, side, id) order
     }
 }
 
@@ -215,44 +223,64 @@ void build_v3_layout_gpu(pq_index_s* idx, cudaStream_t st) {
         d_stored = db.alloc<uint8_t>((size_t)m * 256);
         PQ_CUDA(cudaMemcpyAsync(d_color, color.data(), color.size(), cudaMemcpyHostToDevice, st));
         PQ_CUDA(cudaMemcpyAsync(d_stored, stored.data(), stored.size(), cudaMemcpyHostToDevice, st));
-        // 3-4. signatures over the first sm splits, (class, side) tickets
+        // 3-4. signatures over the first sm splits; items stably sorted by (class, side)
         const int sm = m < 20 ? m : 20;
         const uint32_t mask = (1u << sm) - 1u;
         const uint32_t ncls = 1u << (sm - 1);          // min(s, ~s) has its top bit clear
+        const uint32_t nkey = 2 * ncls;
         uint32_t* d_sig = db.alloc<uint32_t>((size_t)N);
-        uint32_t* d_rank = db.alloc<uint32_t>((size_t)N);
-        unsigned int* d_cnt = db.alloc<unsigned int>((size_t)2 * ncls);
-        PQ_CUDA(cudaMemsetAsync(d_cnt, 0, (size_t)2 * ncls * 4, st));
+        uint32_t* d_key = db.alloc<uint32_t>((size_t)N);
+        uint32_t* d_key2 = db.alloc<uint32_t>((size_t)N);
+        int32_t* d_val = db.alloc<int32_t>((size_t)N);
+        int32_t* d_val2 = db.alloc<int32_t>((size_t)N);
+        unsigned int* d_cnt = db.alloc<unsigned int>(nkey);
+        PQ_CUDA(cudaMemsetAsync(d_cnt, 0, (size_t)nkey * 4, st));
         k0_sig<<<grid_for(N, sms), 256, 0, st>>>(idx->d_codes, N, mp, sm, d_color, d_sig);
-        k0_rank<<<grid_for(N, sms), 256, 0, st>>>(d_sig, N, mask, ncls, d_cnt, d_rank);
+        k0_classkey<<<grid_for(N, sms), 256, 0, st>>>(d_sig, N, mask, d_key, d_val, d_cnt);
         count_launch(2);
-        check_launch("k0_sig / k0_rank");
-        // 5. pair offsets per class
-        std::vector<unsigned int> cnt((size_t)2 * ncls), off(ncls);
+        check_launch("k0_sig / k0_classkey");
+        {
+            size_t tmp_bytes = 0;
+            PQ_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, d_key, d_key2, d_val, d_val2, (int)N, 0, sm,
+                                                    st));
+            void* d_tmp = db.alloc<unsigned char>(tmp_bytes);
+            PQ_CUDA(cub::DeviceRadixSort::SortPairs(d_tmp, tmp_bytes, d_key, d_key2, d_val, d_val2, (int)N, 0, sm,
+                                                    st));
+            count_launch();
+        }
+        // 5. group starts, pair offsets per class, leftover offsets per group
+        std::vector<unsigned int> cnt(nkey);
         PQ_CUDA(cudaMemcpyAsync(cnt.data(), d_cnt, cnt.size() * 4, cudaMemcpyDeviceToHost, st));
         PQ_CUDA(cudaStreamSynchronize(st));
-        int64_t P = 0;
+        std::vector<int64_t> gstart(nkey), poff(ncls), loff(nkey);
+        int64_t P = 0, G0 = 0, L0 = 0;
         for (uint32_t c = 0; c < ncls; ++c) {
-            off[c] = (unsigned int)P;
-            P += std::min(cnt[c], cnt[ncls + c]);
+            const int64_t n0 = cnt[2 * c], n1 = cnt[2 * c + 1], np = std::min(n0, n1);
+            gstart[2 * c] = G0; gstart[2 * c + 1] = G0 + n0; G0 += n0 + n1;
+            poff[c] = P; P += np;
+            loff[2 * c] = L0; loff[2 * c + 1] = L0 + (n0 - np); L0 += (n0 - np) + (n1 - np);
         }
         matched = P;
         leftover = N - 2 * P;
-        unsigned int* d_off = db.alloc<unsigned int>(ncls);
-        PQ_CUDA(cudaMemcpyAsync(d_off, off.data(), off.size() * 4, cudaMemcpyHostToDevice, st));
+        int64_t* d_gstart = db.alloc<int64_t>(nkey);
+        int64_t* d_poff = db.alloc<int64_t>(ncls);
+        int64_t* d_loff = db.alloc<int64_t>(nkey);
+        PQ_CUDA(cudaMemcpyAsync(d_gstart, gstart.data(), gstart.size() * 8, cudaMemcpyHostToDevice, st));
+        PQ_CUDA(cudaMemcpyAsync(d_poff, poff.data(), poff.size() * 8, cudaMemcpyHostToDevice, st));
+        PQ_CUDA(cudaMemcpyAsync(d_loff, loff.data(), loff.size() * 8, cudaMemcpyHostToDevice, st));
         // 6. matched items -> rows 0 .. 2P-1, the rest -> leftover list
         const int64_t max_rows = align_up((size_t)(2 * P + leftover + 1), (size_t)TR);
         d_rowitem = db.alloc<int32_t>((size_t)max_rows);
         PQ_CUDA(cudaMemsetAsync(d_rowitem, 0xFF, (size_t)max_rows * 4, st));
         int32_t* d_left = db.alloc<int32_t>((size_t)std::max<int64_t>(leftover, 1));
-        unsigned int* d_nleft = db.alloc<unsigned int>(1);
-        PQ_CUDA(cudaMemsetAsync(d_nleft, 0, 4, st));
-        k0_emit<<<grid_for(N, sms), 256, 0, st>>>(d_sig, d_rank, N, mask, ncls, d_cnt, d_off, d_rowitem, d_left,
-                                                  d_nleft);
+        k0_emit<<<grid_for(N, sms), 256, 0, st>>>(d_key2, d_val2, N, d_cnt, d_gstart, d_poff, d_loff, d_rowitem,
+                                                  d_left);
         count_launch();
         check_launch("k0_emit");
-        // 7. leftovers on the host: sorted by (signature, id) -- a deterministic
-        // order -- then pairs whose signatures differ from a complement in one
+        // 7. leftovers on the host, in the round-1 builder's order (signature
+        // classes ascending; a class with one side present at that side's
+        // signature; inside a class the smaller signature's items first, ids
+        // ascending): pairs whose signatures differ from a complement in one
         // split (conflict on that split only), then the rest pairwise
         std::vector<int32_t> left((size_t)leftover);
         std::vector<uint32_t> lsig((size_t)leftover);
@@ -267,9 +295,11 @@ void build_v3_layout_gpu(pq_index_s* idx, cudaStream_t st) {
         }
         std::vector<int64_t> ord((size_t)leftover);
         std::iota(ord.begin(), ord.end(), (int64_t)0);
-        std::sort(ord.begin(), ord.end(), [&](int64_t x, int64_t y) {
-            return lsig[x] != lsig[y] ? lsig[x] < lsig[y] : left[x] < left[y];
-        });
+        auto visit = [&](int64_t x) -> uint32_t {       // (the list arrives in (class, side, id) order)
+            const uint32_t sg = lsig[x], cls = std::min(sg, sg ^ mask);
+            return (cnt[2 * cls] > 0 && cnt[2 * cls + 1] > 0) ? cls : sg;
+        };
+        std::stable_sort(ord.begin(), ord.end(), [&](int64_t x, int64_t y) { return visit(x) < visit(y); });
         std::vector<int32_t> lrows;                   // rows 2P .. in pairs
         lrows.reserve((size_t)leftover + 1);
         {

@@ -149,7 +149,8 @@ void launch_subscores(const float* phi, const float* psi, int B, int d, int m, i
     // users per block: 32 for batches (a staged psi tile serves 32 users), fewer
     // for small B; PQTOPK_K1_UB forces one (diagnostics A/B)
     static const int forced = [] { const char* e = getenv("PQTOPK_K1_UB"); return e ? atoi(e) : 0; }();
-    const int ub = forced ? forced : (B >= 32 ? 32 : B >= 16 ? 16 : B >= 8 ? 8 : 4);
+    // (measured, r02: C2 B = 128: 32 -> 14.8 us vs 16.8 at 4-16; C3 / C4: 16 best, 25 / 72 us)
+    const int ub = forced ? forced : (B > 128 ? 16 : B >= 32 ? 32 : B >= 16 ? 16 : B >= 8 ? 8 : 4);
     switch (ub) {
         case 32: launch_k1<32>(phi, psi, B, d, m, b, S, st); break;
         case 16: launch_k1<16>(phi, psi, B, d, m, b, S, st); break;
