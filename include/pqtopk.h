@@ -204,13 +204,21 @@ pq_status pq_score_topk(pq_index idx, const float* S, int32_t B, int32_t K,
  *   V   : int32 [nV], device; LOCAL item ids (0 <= V[r] < N), strictly
  *         increasing; shared by the B users.  nV == 0: every row is padding.
  *   other arguments as pq_score_topk (ids returned are global ids).
- * Validates V on the device and synchronises `stream` (PQ_ERR_INVALID_ARG
+ * Asynchronous and graph-capturable (enqueues only; nV == 0 fills the padding
+ * on the device).  V is NOT validated: an entry outside [0, N) is read as code
+ * 0 (memory-safe) and a V that is not strictly increasing gives an undefined
+ * (but memory-safe) answer.  Pass PQ_SUBSET_VALIDATE to pq_score_topk_subset_ex
+ * to check V on the device first (synchronises `stream`; PQ_ERR_INVALID_ARG
  * names the first bad position).  Workspace: pq_subset_workspace_bytes.
  */
 size_t pq_subset_workspace_bytes(pq_index idx, int64_t nV, int32_t B, int32_t K);
 pq_status pq_score_topk_subset(pq_index idx, const float* S, int32_t B, int32_t K,
                                const int32_t* V, int64_t nV, void* ws, size_t ws_bytes,
                                int32_t* ids, float* scores, void* stream);
+#define PQ_SUBSET_VALIDATE 1
+pq_status pq_score_topk_subset_ex(pq_index idx, const float* S, int32_t B, int32_t K,
+                                  const int32_t* V, int64_t nV, int32_t flags, void* ws,
+                                  size_t ws_bytes, int32_t* ids, float* scores, void* stream);
 
 /*
  * pq_score_topk_exclude — PQTopK over I minus a per-user exclusion list (e.g.

@@ -32,7 +32,7 @@ EXPORTS = ["pq_abi_version", "pq_last_error", "pq_launch_count", "pq_create", "p
            "pq_score_topk", "pq_search_workspace_bytes", "pq_search", "pq_search_ex", "pq_search_plan_info", "pq_merge_workspace_bytes",
            "pq_merge_topk", "pq_merge_topk_packed", "pq_reconstruct", "pq_dense_workspace_bytes", "pq_dense_topk",
            "pq_recjpq_workspace_bytes", "pq_recjpq_topk", "pq_timing_enable", "pq_timing_read",
-           "pq_subset_workspace_bytes", "pq_score_topk_subset", "pq_exclude_workspace_bytes",
+           "pq_subset_workspace_bytes", "pq_score_topk_subset", "pq_score_topk_subset_ex", "pq_exclude_workspace_bytes",
            "pq_score_topk_exclude"]
 
 
@@ -84,6 +84,7 @@ def load_library():
         "pq_score_topk": (st, [P, P, I32, I32, P, SZ, P, P, P]),
         "pq_subset_workspace_bytes": (SZ, [P, I64, I32, I32]),
         "pq_score_topk_subset": (st, [P, P, I32, I32, P, I64, P, SZ, P, P, P]),
+        "pq_score_topk_subset_ex": (st, [P, P, I32, I32, P, I64, I32, P, SZ, P, P, P]),
         "pq_exclude_workspace_bytes": (SZ, [P, I32, I32, I32]),
         "pq_score_topk_exclude": (st, [P, P, I32, I32, P, P, I32, P, SZ, P, P, P]),
         "pq_search_workspace_bytes": (SZ, [P, I32, I32, I32]),
@@ -304,9 +305,11 @@ def pq_score_topk(index: PQIndex, S, K: int, ws=None, ids=None, scores=None, str
     return ids, scores
 
 
-def pq_score_topk_subset(index: PQIndex, S, K: int, V, ws=None, ids=None, scores=None, stream=None):
+def pq_score_topk_subset(index: PQIndex, S, K: int, V, ws=None, ids=None, scores=None, stream=None,
+                         validate: bool = False):
     """PQTopK over the item subset V (Alg. 1 input V): V = sorted unique
-    LOCAL item ids (int32 CUDA tensor), shared by the batch."""
+    LOCAL item ids (int32 CUDA tensor), shared by the batch.  Asynchronous;
+    validate=True checks V on the device first (synchronises, raises PQError)."""
     torch = _torch()
     _need_cuda(S, "S")
     B = int(S.shape[0])
@@ -320,9 +323,9 @@ def pq_score_topk_subset(index: PQIndex, S, K: int, V, ws=None, ids=None, scores
     L = load_library()
     nb = int(L.pq_subset_workspace_bytes(index.handle, nV, B, K)) if B > 0 and 0 < K <= MAX_K and nV > 0 else 0
     ws, wsb = _ws(nb, ws, dev)
-    _check(L.pq_score_topk_subset(index.handle, ctypes.c_void_p(_ptr(S)), B, K,
-                                  ctypes.c_void_p(_ptr(V) if nV else 0), nV,
-                                  ctypes.c_void_p(_ptr(ws) if ws is not None else 0), wsb,
+    _check(L.pq_score_topk_subset_ex(index.handle, ctypes.c_void_p(_ptr(S)), B, K,
+                                     ctypes.c_void_p(_ptr(V) if nV else 0), nV, 1 if validate else 0,
+                                     ctypes.c_void_p(_ptr(ws) if ws is not None else 0), wsb,
                                   ctypes.c_void_p(_ptr(ids)), ctypes.c_void_p(_ptr(scores)),
                                   ctypes.c_void_p(_stream(stream))))
     return ids, scores

@@ -17,15 +17,32 @@
 
 namespace pq {
 
-__global__ void k5_gather_codes(const uint8_t* __restrict__ codes, int mp, const int32_t* __restrict__ V,
+// (an entry of V outside [0, N) -- a caller error the asynchronous call does
+// not detect -- is read as code 0: memory-safe)
+__global__ void k5_gather_codes(const uint8_t* __restrict__ codes, int mp, int64_t N, const int32_t* __restrict__ V,
                                 int64_t nV, uint8_t* __restrict__ out) {
     const int64_t total = nV * mp;
     for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < total;
          x += (int64_t)gridDim.x * blockDim.x) {
         const int64_t r = x / mp;
         const int k = (int)(x - r * mp);
-        out[x] = codes[(int64_t)V[r] * mp + k];
+        const int32_t v = V[r];
+        out[x] = (v >= 0 && v < N) ? codes[(int64_t)v * mp + k] : (uint8_t)0;
     }
+}
+
+__global__ void k5_fill_padding(int32_t* __restrict__ ids, float* __restrict__ scores, int64_t n) {
+    for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < n; x += (int64_t)gridDim.x * blockDim.x) {
+        ids[x] = -1;
+        scores[x] = -INFINITY;
+    }
+}
+
+void launch_fill_padding(int32_t* ids, float* scores, int64_t n, cudaStream_t st) {
+    const int blocks = (int)std::min<int64_t>(std::max<int64_t>(1, ceil_div(n, 256)), 148 * 8);
+    k5_fill_padding<<<blocks, 256, 0, st>>>(ids, scores, n);
+    count_launch();
+    check_launch("k5_fill_padding");
 }
 
 __global__ void k5_check_subset(const int32_t* __restrict__ V, int64_t nV, int64_t N,
@@ -37,10 +54,10 @@ __global__ void k5_check_subset(const int32_t* __restrict__ V, int64_t nV, int64
     }
 }
 
-void launch_gather_codes(const uint8_t* codes, int mp, const int32_t* V, int64_t nV, uint8_t* out,
+void launch_gather_codes(const uint8_t* codes, int mp, int64_t N, const int32_t* V, int64_t nV, uint8_t* out,
                          cudaStream_t st) {
     const int blocks = (int)std::min<int64_t>(std::max<int64_t>(1, ceil_div(nV * mp, 256)), 148 * 16);
-    k5_gather_codes<<<blocks, 256, 0, st>>>(codes, mp, V, nV, out);
+    k5_gather_codes<<<blocks, 256, 0, st>>>(codes, mp, N, V, nV, out);
     count_launch();
     check_launch("k5_gather_codes");
 }

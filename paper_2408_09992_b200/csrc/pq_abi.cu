@@ -725,36 +725,42 @@ size_t pq_subset_workspace_bytes(pq_index idx, int64_t nV, int32_t B, int32_t K)
 pq_status pq_score_topk_subset(pq_index idx, const float* S, int32_t B, int32_t K, const int32_t* V,
                                int64_t nV, void* ws, size_t ws_bytes, int32_t* ids, float* scores,
                                void* stream) {
+    return pq_score_topk_subset_ex(idx, S, B, K, V, nV, 0, ws, ws_bytes, ids, scores, stream);
+}
+
+pq_status pq_score_topk_subset_ex(pq_index idx, const float* S, int32_t B, int32_t K, const int32_t* V,
+                                  int64_t nV, int32_t flags, void* ws, size_t ws_bytes, int32_t* ids,
+                                  float* scores, void* stream) {
     PQ_API_BEGIN
     need(idx != nullptr, "index is NULL");
     check_topk_args(B, K);
     need(nV >= 0, "nV must be >= 0");
+    need((flags & ~PQ_SUBSET_VALIDATE) == 0, "unknown pq_score_topk_subset_ex flags");
     if (B == 0 || K == 0) return PQ_OK;
     need(S && ids && scores, "NULL pointer");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    if (nV == 0) {                                     // empty subset: all padding (R11)
-        std::vector<int32_t> hi((size_t)B * K, -1);
-        std::vector<float> hs((size_t)B * K, -INFINITY);
-        PQ_CUDA(cudaMemcpyAsync(ids, hi.data(), hi.size() * 4, cudaMemcpyHostToDevice, st));
-        PQ_CUDA(cudaMemcpyAsync(scores, hs.data(), hs.size() * 4, cudaMemcpyHostToDevice, st));
-        PQ_CUDA(cudaStreamSynchronize(st));
+    if (nV == 0) {                                     // empty subset: all padding (R11), on the device
+        launch_fill_padding(ids, scores, (int64_t)B * K, st);
         return PQ_OK;
     }
-    need(V != nullptr && is_device_ptr(V), "V must be a device array of nV item ids");
+    need(V != nullptr, "V is NULL");
     const size_t nb = pq_subset_workspace_bytes(idx, nV, B, K);
     if (!ws || ws_bytes < nb) fail(PQ_ERR_WORKSPACE, "workspace too small: need " + std::to_string(nb) + " bytes");
     Carve c(ws);
     uint8_t* codesV = c.take<uint8_t>((size_t)nV * idx->lay.mp + 64);
     unsigned long long* bad = c.take<unsigned long long>(8);
-    PQ_CUDA(cudaMemsetAsync(bad, 0xFF, 8, st));
-    launch_check_subset(V, nV, idx->N, bad, st);
-    unsigned long long hbad = 0;
-    PQ_CUDA(cudaMemcpyAsync(&hbad, bad, 8, cudaMemcpyDeviceToHost, st));
-    PQ_CUDA(cudaStreamSynchronize(st));
-    if (hbad != ~0ull)
-        fail(PQ_ERR_INVALID_ARG, "V must hold strictly increasing local item ids in [0, N): first bad "
-                                 "position " + std::to_string(hbad));
-    launch_gather_codes(idx->d_codes, idx->lay.mp, V, nV, codesV, st);
+    if (flags & PQ_SUBSET_VALIDATE) {                  // debug / untrusted V: synchronous check
+        need(is_device_ptr(V), "V must be a device array of nV item ids");
+        PQ_CUDA(cudaMemsetAsync(bad, 0xFF, 8, st));
+        launch_check_subset(V, nV, idx->N, bad, st);
+        unsigned long long hbad = 0;
+        PQ_CUDA(cudaMemcpyAsync(&hbad, bad, 8, cudaMemcpyDeviceToHost, st));
+        PQ_CUDA(cudaStreamSynchronize(st));
+        if (hbad != ~0ull)
+            fail(PQ_ERR_INVALID_ARG, "V must hold strictly increasing local item ids in [0, N): first bad "
+                                     "position " + std::to_string(hbad));
+    }
+    launch_gather_codes(idx->d_codes, idx->lay.mp, idx->N, V, nV, codesV, st);
     pq_index_s t = subset_index(idx, nV, codesV, V);
     run_score_topk(&t, S, B, K, c.base + c.off, ws_bytes - c.off, ids, scores, st);
     PQ_API_END

@@ -214,8 +214,9 @@ void k3_rows_to_keys(const float* R, int64_t ld, int64_t n, int B, int K, uint32
                      cudaStream_t st);
 
 // K5 (k5_subset.cu): item subsets and exclusion lists
-void launch_gather_codes(const uint8_t* codes, int mp, const int32_t* V, int64_t nV, uint8_t* out,
+void launch_gather_codes(const uint8_t* codes, int mp, int64_t N, const int32_t* V, int64_t nV, uint8_t* out,
                          cudaStream_t st);
+void launch_fill_padding(int32_t* ids, float* scores, int64_t n, cudaStream_t st);
 void launch_check_subset(const int32_t* V, int64_t nV, int64_t N, unsigned long long* first_bad,
                          cudaStream_t st);
 void launch_exclude(const int32_t* ids2, const float* sc2, int B, int K2, const int32_t* excl,

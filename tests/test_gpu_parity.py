@@ -513,8 +513,25 @@ def test_subset_parity(pq, torch, orc, case):
     ri, rs = orc.pq_topk(G[V], S_t.cpu().numpy(), K)          # V ascending: row order = id order
     ri = np.where(ri >= 0, V[np.clip(ri, 0, None)] + base, -1).astype(np.int32)
     assert_same(ids.cpu().numpy(), sc.cpu().numpy(), ri, rs)
-    with pytest.raises(pq.PQError):                            # V must be strictly increasing
-        pq.pq_score_topk_subset(idx, S_t, K, torch.from_numpy(V[::-1].copy()).cuda())
+    with pytest.raises(pq.PQError):                            # V must be strictly increasing (validated call)
+        pq.pq_score_topk_subset(idx, S_t, K, torch.from_numpy(V[::-1].copy()).cuda(), validate=True)
+    # the asynchronous call is graph-capturable and equals the validated one
+    vi, vs = pq.pq_score_topk_subset(idx, S_t, K, torch.from_numpy(V).cuda(), validate=True)
+    assert_same(vi.cpu().numpy(), vs.cpu().numpy(), ri, rs)
+    Vd = torch.from_numpy(V).cuda()
+    ws = torch.empty(max(1, int(pq.load_library().pq_subset_workspace_bytes(idx.handle, len(V), B, K))),
+                     dtype=torch.uint8, device="cuda")
+    gi = torch.empty((B, K), dtype=torch.int32, device="cuda")
+    gs = torch.empty((B, K), dtype=torch.float32, device="cuda")
+    pq.pq_score_topk_subset(idx, S_t, K, Vd, ws=ws, ids=gi, scores=gs)      # warm (plans, attributes)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        pq.pq_score_topk_subset(idx, S_t, K, Vd, ws=ws, ids=gi, scores=gs)
+    gi.fill_(7); gs.fill_(0.0)
+    g.replay()
+    torch.cuda.synchronize()
+    assert_same(gi.cpu().numpy(), gs.cpu().numpy(), ri, rs)
 
 
 @pytest.mark.parametrize("B,K,dist", [(2, 10, "uniform"), (24, 100, "uniform"), (5, 64, "few")])
