@@ -24,7 +24,7 @@ if [ -n "$TRACE" ]; then
   PQTOPK_NVCC_EXTRA=-DK6_TRACE python -m paper_2408_09992_b200.build --force > /dev/null 2>&1
   for c in ${TRACE}; do
     timeout 600 python scripts/trace_k6_run.py $c gpurun_out/k6_${c}_${TAG}.trace > /dev/null 2>&1
-    python scripts/trace_k6.py gpurun_out/k6_${c}_${TAG}.trace px > gpurun_out/trace_${c}_${TAG}.txt 2>&1
+    python scripts/trace_k6.py gpurun_out/k6_${c}_${TAG}.trace > gpurun_out/trace_${c}_${TAG}.txt 2>&1
     echo "== trace $c"; cat gpurun_out/trace_${c}_${TAG}.txt
   done
 fi

@@ -26,7 +26,3 @@ raw_i = np.frombuffer(raw[8:], np.int64).reshape(grid, n)
 last = raw_i[:, 6] > 0
 print("  merge CTA(s): n3 =", raw_i[last, 31].tolist(), " floor key =", [hex(x & 0xFFFFFFFFFFFFFFFF) for x in raw_i[last, 30].tolist()])
 print("  chunk candidates at the end (min/median/max):", int(raw_i[:, 29].min()), int(np.median(raw_i[:, 29])), int(raw_i[:, 29].max()))
-if len(sys.argv) > 2 and sys.argv[2] == "px":     # prefix-mode counters (grid mode)
-    for i, nm in ((24, "full rounds"), (25, "queue rounds"), (26, "survivors queued"), (27, "pmin solves")):
-        v = raw_i[:, i]
-        print(f"  {nm:18s} min {int(v.min())} median {int(np.median(v))} max {int(v.max())} total {int(v.sum())}")
