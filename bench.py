@@ -144,12 +144,24 @@ def workload_name(cfg):
             f"codes={cfg.codes}")
 
 
+def oracle_all_cores():
+    """The oracle on every host core this process may use (torchrun exports
+    OMP_NUM_THREADS=1 to its ranks; the CPU baseline wants the whole host)."""
+    import oracle
+    try:
+        n = len(os.sched_getaffinity(0))
+    except AttributeError:                           # pragma: no cover - non-Linux
+        n = os.cpu_count() or 1
+    oracle.set_threads(n)
+    return oracle
+
+
 def cpu_oracle_sample(cfg, codes, S_host, gpu_ids, gpu_sc, budget_s=12.0, max_users=64):
     """Time the CPU oracle (Alg. 1, plain C + OpenMP) on a bounded sample of
     users over the full catalogue -- users spread over the whole batch
     (parity_users) -- and check those users bit-exactly against the GPU result.
     Also times one user with ONE thread (the per-core figure)."""
-    import oracle
+    oracle = oracle_all_cores()
     users = parity_users(cfg.B, max_users)
     done, t_tot, exact, checked = 0, 0.0, 0, []
     for u in users:
@@ -190,7 +202,7 @@ def run_reference(args):
     world, rank, _ = dist_env()
     if rank != 0:
         return
-    import oracle
+    oracle = oracle_all_cores()
     cfg = pqsynth.CONFIGS[args.config]
     codes = pqsynth.codes(cfg)
     P = pqsynth.psi(cfg)
