@@ -319,8 +319,9 @@ def run_ours(args):
             tun["variant"] = args.variant
         idx.set_tuning(**tun)
     # B <= 4 (the serving case): pq_search runs the whole path as ONE fused
-    # kernel (K6: sub-id scores + gather-sum + select + merge); that call is the step
-    fused = args.fused == "on" and idx.search_plan(B, d, K)["variant"] == 5
+    # kernel (K7 with chunk-resident codes, else K6 with a streamed code ring:
+    # sub-id scores + gather-sum + select + merge); that call is the step
+    fused = args.fused == "on" and idx.search_plan(B, d, K)["variant"] in (5, 7)
     plan = idx.search_plan(B, d, K) if fused else idx.plan(B, K)
     layout = idx.layout()
 
@@ -514,7 +515,9 @@ def run_ours(args):
     kname = {1: "k2_score_select (v1 row groups)",
              3: "k2_tiled (v3: fused gather-sum-select, 4 users/lane)",
              4: "k2_latency (v4: small-batch fused gather-sum-select)",
-             5: "k6_query (K1 + gather-sum + select + merge in one launch, B <= 4)"}.get(plan["variant"], "k2")
+             5: "k6_query (K1 + gather-sum + select + merge in one launch, B <= 4; streamed code ring)",
+             7: "k7_resident (K1 + gather-sum + select + merge in one launch, B <= 4; chunk-resident codes)"
+             }.get(plan["variant"], "k2")
     common = {
         "kernel": kname, "traffic": traffic,
         "per_launch": {"lookups": lookups, "algorithmic_hbm_bytes": hbm_bytes, "k2_ms": k2_avg_s * 1e3},
@@ -616,7 +619,7 @@ def main():
     ap.add_argument("--compare", default="auto", choices=["auto", "on", "off"],
                     help="time the paper's baselines beside PQTopK (auto: c2, c3)")
     ap.add_argument("--variant", type=int, default=0,
-                    help="force the K2 variant (1 row groups, 3 tiled, 4 small batch; 5 = fused K6 in pq_search; 0 = auto)")
+                    help="force the K2 variant (1 row groups, 3 tiled, 4 small batch; 5 = fused K6 / 7 = fused K7 in pq_search; 0 = auto)")
     ap.add_argument("--graph", default="auto", choices=["auto", "on", "off"],
                     help="replay the step as a CUDA graph (auto: single GPU)")
     ap.add_argument("--no-flush", action="store_true", help="diagnostics: skip the L2 flush (not a valid bench line)")

@@ -72,8 +72,11 @@ typedef struct {
                             superseded paired half-warp kernel; treated as auto);
                             3 = tiled phases (4 users per lane, TMA tables, TMEM partials);
                             4 = small-batch latency kernel (B <= 4, lane = item);
-                            pq_search only: 5 = the fused single-launch query kernel (K6,
-                            B <= 4); 0 lets pq_search pick K6 whenever it applies */
+                            pq_search only: 5 = the fused single-launch query kernel with a
+                            streamed code ring (K6, B <= 4); 7 = the fused single-launch
+                            kernel with each CTA's code chunk resident in shared memory
+                            (K7, B <= 4, catalogues whose chunks fit); 0 lets pq_search pick
+                            K7, else K6, whenever one applies */
     int32_t ctas;        /* persistent CTAs of the scoring kernel (0 = #SMs x occupancy) */
     int32_t warps;       /* warps per CTA of the scoring kernel (0 = auto) */
     int32_t chunks;      /* item chunks per user group (0 = auto) */
@@ -156,7 +159,7 @@ pq_status pq_plan_info(pq_index idx, int32_t B, int32_t K, int64_t out[8]);
 
 /*
  * The plan pq_search would use for (B, d, K): out[0] = 5 when the fused K6
- * kernel runs (then out[1] table copies G, out[2] CTAs per cluster (0: one
+ * kernel runs, 7 when the fused chunk-resident K7 kernel runs (then out[1] table copies G, out[2] CTAs per cluster (0: one
  * cooperative grid sharing S through L2), out[3]
  * warps per CTA, out[4] CTAs, out[5] item chunks per user, out[6] 0, out[7]
  * dynamic shared memory bytes), else exactly pq_plan_info(B, K).

@@ -840,7 +840,10 @@ bool k6_query_plan(pq_index_s* idx, int B, int d, int K, K6Plan& p) {
             p = e.p;
             return e.ok;
         }
-    const bool ok = plan_uncached(idx, B, d, K, p);
+    // K7 (codes of each CTA's chunk resident in shared memory) whenever it
+    // applies, unless the tuning forces K6 (variant 5); K6 otherwise
+    bool ok = idx->tuning.variant == 7 && k7_resident_plan(idx, B, d, K, p);   // (auto: K6 until K7 is faster)
+    if (!ok && idx->tuning.variant != 7) ok = plan_uncached(idx, B, d, K, p);
     v->push_back(K6CacheEnt{B, d, K, idx->tuning, ok, p});
     return ok;
 }
@@ -852,12 +855,17 @@ void k6_cache_free(pq_index_s* idx) {
 }
 
 size_t k6_query_ws_bytes(const K6Plan& p, int B, int E) {
+    if (p.resident) return k7_resident_ws_bytes(p, B, E);
     return align_up(p.cand_bytes, 256) + 2 * align_up((size_t)B * p.chunks * 8, 256) +
            align_up((size_t)(B + 1) * 4, 256) + align_up((size_t)B * E * 4, 256);
 }
 
 void launch_k6_query(const pq_index_s* idx, const K6Plan& p, const float* phi, const float* psi, int B,
                      int d, int K, void* ws, float* S_out, int32_t* ids, float* scores, cudaStream_t st) {
+    if (p.resident) {
+        launch_k7_resident(idx, p, phi, psi, B, d, K, ws, S_out, ids, scores, st);
+        return;
+    }
     K6Args a{};
     a.codes = idx->d_codes;
     a.perm = idx->lay.paired ? idx->d_perm : nullptr;

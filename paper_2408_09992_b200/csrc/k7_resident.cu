@@ -1,0 +1,659 @@
+// K7 — the whole hot path of one small batch (B <= 4: the paper's serving case,
+// one user per query; mRT below ~1e6 items) in ONE launch, for
+// catalogues whose per-CTA share of the code matrix fits in shared memory
+// (m = 8: up to ~1.8M items on 148 SMs; C1, C2a).  Latency-first design:
+//
+//   (0) each CTA issues ONE bulk TMA copy of its whole item chunk's code rows
+//       (no ring, no refills) before anything else, so the HBM stream of the
+//       codes overlaps the sub-id score phase;
+//   (1) S (Eq. 4): the grid splits the B*m*b entries evenly, four
+//       threads per entry, one fp64 fma chain each over t = j (mod 4), combined
+//       as (c0 + c1) + (c2 + c3) and rounded to fp32 once — K1's order (R5b),
+//       so S is bit-identical to pq_subscores.  Each entry is published as ONE
+//       64-bit word (1 << 32 | fp32 bits): the word is its own ready flag, so a
+//       reader polls exactly the entries it needs and no grid barrier, fence or
+//       counter round trip sits between the producer and the consumers
+//       (cooperative launch: every CTA is resident);
+//   (2) each CTA polls its user's E = m*b words and writes G copies of the
+//       table into shared memory (lane l reads copy l mod G);
+//   (3) r_ui (Eq. 5, Alg. 1): thread t scores items t + 512 j of the
+//       resident chunk, split-major over its J items (J independent fp32 add
+//       chains in the sequential order j = 0..m-1, R1), scores kept in
+//       registers;
+//   (4) the chunk's exact top-K (R3 key: score desc, id asc): a proved floor
+//       (the K-th largest of the per-warp top-min(K,32) thread maxima — K
+//       distinct items reach it), keys only for the items that reach it,
+//       ranked all-pairs (or radix-selected when many);
+//   (5) each chunk writes its sorted list and K-th key to fixed slots; the last
+//       CTA of the user (one ticket atomic) takes floor = max chunk K-th key
+//       (that chunk alone holds K keys >= it), keeps the keys >= floor, ranks
+//       them and writes ids / scores.
+//
+// The tagged S words and the tickets live in the call's workspace and are
+// zeroed by the one-CTA k7_reset kernel launched before K7 as its programmatic
+// dependent (griddepcontrol.wait precedes the first access to them).
+#include "k2_common.cuh"
+#include "ptx_dev.cuh"
+#include <mutex>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+
+namespace pq {
+
+struct K7Args {
+    const uint8_t* codes;          // [N][mp] item-order rows (K0 layout, >= 16 bytes of tail pad)
+    const float* phi;              // [B][d]
+    const float* psi;              // [m][b][L], L = d / m
+    float* S_out;                  // optional [B][m][b] copy of the sub-id scores
+    unsigned long long* Sx;        // [B][E] tagged sub-id scores (zeroed by k7_reset)
+    unsigned int* done;            // [B] finished-chunk tickets (zeroed by k7_reset)
+    uint64_t* cand;                // [B][chunks][K] per-chunk sorted lists
+    int32_t* ids;                  // [B][K]
+    float* scores;                 // [B][K]
+    long long* trace;              // diagnostics (-DK6_TRACE + PQTOPK_K6_TRACE): [grid][32] stamps
+    int64_t N;
+    int mp, b, B, K, d, L;
+    uint32_t id_base;
+    int chunks;                    // per user
+    int chunk_items;               // multiple of 16, <= K7_THREADS * K7_JMAX
+};
+
+constexpr int K7_THREADS = 512;
+constexpr int K7_NWARP = K7_THREADS / 32;
+constexpr int K7_JMAX = 24;        // items per thread
+constexpr int K7_MAXK = 512;
+
+// Helpers are out of line: the chunk phase runs them first, so the last CTA's
+// merge finds their code in the instruction cache (a once-per-launch path is
+// otherwise fetched cold).
+
+// one key per lane, bitonic across the warp, descending (lane 0 = largest)
+__device__ __noinline__ uint64_t k7_warp_sort_desc(uint64_t v) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int k = 2; k <= 32; k <<= 1)
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            const uint64_t o = __shfl_xor_sync(FULL, v, j);
+            const bool desc = (lane & k) == 0, lower = (lane & j) == 0;
+            v = (lower == desc) ? (o > v ? o : v) : (o < v ? o : v);
+        }
+    return v;
+}
+
+__device__ __noinline__ uint64_t k7_block_kth(const uint64_t* buf, int n, uint32_t K, uint32_t* hist,
+                                              unsigned long long* sc) {
+    return block_kth(buf, n, K, hist, sc);
+}
+
+// Rank of `mine` among buf[0..n) (keys unique; 0 = empty never outranks):
+// the number of keys above it.  Eight independent 128-bit broadcast loads in
+// flight (the loop is load-latency bound otherwise).  buf 16-byte aligned.
+__device__ __noinline__ int k7_rank(const uint64_t* buf, int n, uint64_t mine) {
+    int r0 = 0, r1 = 0;
+    int j = 0;
+    for (; j + 16 <= n; j += 16) {
+        ulonglong2 v[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) v[q] = *reinterpret_cast<const ulonglong2*>(buf + j + 2 * q);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) { r0 += v[q].x > mine ? 1 : 0; r1 += v[q].y > mine ? 1 : 0; }
+    }
+    for (; j < n; ++j) r0 += buf[j] > mine ? 1 : 0;
+    return r0 + r1;
+}
+
+__device__ __forceinline__ uint64_t k7_warp_max(uint64_t v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        const uint64_t t = __shfl_xor_sync(FULL, v, o);
+        v = t > v ? t : v;
+    }
+    return v;
+}
+
+// Warp-aggregated append of `key` (if keep) to buf at the shared counter.
+__device__ __forceinline__ void k7_append(bool keep, uint64_t key, uint64_t* buf, int* count) {
+    const unsigned bm = __ballot_sync(FULL, keep);
+    if (bm) {
+        const int lane = threadIdx.x & 31;
+        int base = 0;
+        if (lane == 0) base = atomicAdd(count, __popc(bm));
+        base = __shfl_sync(FULL, base, 0);
+        if (keep) buf[base + __popc(bm & lanemask_lt())] = key;
+    }
+}
+
+// The exact top-K (sorted) of n unique nonzero keys in smem buf -> out[rank]
+// (global memory) for rank < min(K, n).  n <= 32: warp 0 sorts them; n <= 256:
+// ranked all-pairs; larger: radix-select the K-th key, keep the K keys >= it
+// (into tmp, >= K slots) and rank those.  All threads call it.
+__device__ __noinline__ void k7_topk(const uint64_t* buf, int n, int K, uint64_t* tmp, int* count,
+                                     uint32_t* hist, unsigned long long* sc, uint64_t* out) {
+    const int tid = threadIdx.x;
+    if (n <= 32) {
+        if (tid < 32) {
+            const uint64_t srt = k7_warp_sort_desc(tid < n ? buf[tid] : 0ull);
+            if (tid < n && tid < K) out[tid] = srt;
+        }
+        return;
+    }
+    if (n > 256) {
+        const uint64_t kk = k7_block_kth(buf, n, (uint32_t)K, hist, sc);
+        if (tid == 0) *count = 0;
+        __syncthreads();
+        for (int c0 = 0; c0 < n; c0 += K7_THREADS) {
+            const int i = c0 + tid;
+            const uint64_t v = i < n ? buf[i] : 0ull;
+            k7_append(i < n && v >= kk, v, tmp, count);
+        }
+        __syncthreads();
+        n = *count;                                    // == K (keys are unique)
+        buf = tmp;
+    }
+    for (int i = tid; i < n; i += K7_THREADS) {
+        const uint64_t mine = buf[i];
+        const int rk = k7_rank(buf, n, mine);
+        if (rk < K) out[rk] = mine;
+    }
+}
+
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" :: "l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+
+// Shared memory: [T: M*b*G fp32 | R: codes of the chunk (each row's first 4
+// bytes then hold the item's score), then candidate keys] (dynamic) + fk[1024]
+// keys, hist[256], small scalars (static).  The last CTA of a user reuses T + R
+// as merge scratch (chunks * K keys, checked by the plan).
+template <int M, int G>
+__global__ void __launch_bounds__(K7_THREADS, 1) k7_resident(const K7Args a) {
+    constexpr int MP = (M + 3) / 4 * 4;
+    constexpr int NW = MP / 4;
+    constexpr int JB = 8;                              // items per thread in flight while scoring
+    extern __shared__ __align__(128) unsigned char sm_raw[];
+    __shared__ __align__(16) uint64_t fk[2 * K7_THREADS];
+    __shared__ uint32_t hist[256];
+    __shared__ unsigned long long sc[4];
+    __shared__ unsigned long long floor_key;
+    __shared__ int count;
+    __shared__ int is_last;
+    __shared__ __align__(8) unsigned long long mbar;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int bq = a.b;
+    const int E = M * bq;
+    const int K = a.K;
+    const size_t tb0 = align_up((size_t)E * G * 4, 128), tb1 = (size_t)a.chunk_items * 8;
+    const size_t tbytes = tb0 > tb1 ? tb0 : tb1;
+    float* T = reinterpret_cast<float*>(sm_raw);
+    unsigned char* Rg = sm_raw + tbytes;
+    uint64_t* cbuf = reinterpret_cast<uint64_t*>(sm_raw);   // candidates: over T once scored
+    const int u = blockIdx.x / a.chunks;
+    const int chunk = blockIdx.x - u * a.chunks;
+    const int64_t i0 = (int64_t)chunk * a.chunk_items;
+    const int nit = (int)max((int64_t)0, min((int64_t)a.chunk_items, a.N - i0));
+    const uint32_t cbytes = (uint32_t)align_up((size_t)nit * MP, 16);
+    const uint32_t bar = smem_u32(&mbar);
+    auto stamp = [&](int i) {                          // diagnostics builds only (-DK6_TRACE)
+#ifdef K6_TRACE
+        if (a.trace && tid == 0) {
+            long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            a.trace[(int64_t)blockIdx.x * 32 + i] = t;
+        }
+#else
+        (void)i;
+#endif
+    };
+    stamp(0);
+    // the chunk's code rows -> R in bulk TMA copies on one mbarrier (no ring: the
+    // whole chunk is resident).  Issued by thread 0 right after its own sub-id
+    // score loads, so the sub-id score requests are not queued behind 10 MB of codes.
+    auto issue_codes = [&]() {
+        if (cbytes) {
+            mbar_expect_tx(bar, cbytes);
+            for (uint32_t o = 0; o < cbytes; o += 32768u)
+                bulk_g2s(smem_u32(Rg) + o, a.codes + i0 * MP + o, min(32768u, cbytes - o), bar);
+        }
+    };
+    if (tid == 0) {
+        mbar_init(bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        count = 0;
+        floor_key = 0ull;
+    }
+    bool issued = false;
+
+    // ---- (1) this CTA's share of the B*E sub-id scores, K1's fp64 order (R5b)
+    {
+        const int EB = a.B * E;
+        const int per = (EB + (int)gridDim.x - 1) / (int)gridDim.x;
+        const int e0 = (int)blockIdx.x * per, e1 = min(EB, e0 + per);
+        const int j = tid & 3;
+        for (int base = e0; base < e1; base += K7_THREADS / 4) {
+            const int ent = base + (tid >> 2);
+            const bool ok = ent < e1;
+            const int uu = ok ? ent / E : 0, ee = ok ? ent - uu * E : 0;
+            const float* pr = a.psi + (int64_t)ee * a.L;
+            const float* fr = a.phi + (int64_t)uu * a.d + (int64_t)(ee / bq) * a.L;
+            double x = 0.0;
+            for (int t0 = j; t0 < a.L; t0 += 64) {     // 16 terms of the chain per pass
+                float pv[16], fv[16];
+#pragma unroll
+                for (int q = 0; q < 16; ++q) {
+                    const int t = t0 + 4 * q;
+                    const bool in = ok && t < a.L;
+                    pv[q] = in ? __ldg(pr + t) : 0.0f;
+                    fv[q] = in ? __ldg(fr + t) : 0.0f;
+                }
+                if (tid == 0 && !issued) { issue_codes(); issued = true; }
+#pragma unroll
+                for (int q = 0; q < 16; ++q)
+                    if (t0 + 4 * q < a.L) x = fma((double)pv[q], (double)fv[q], x);
+            }
+            // (c0 + c1) + (c2 + c3): lanes 4e .. 4e + 3 hold c0 .. c3
+            const double x1 = __shfl_down_sync(FULL, x, 1);
+            const double s01 = x + x1;                 // valid in lanes j = 0, 2
+            const double s23 = __shfl_down_sync(FULL, s01, 2);
+            if (base == e0) stamp(1);
+            // the tagged words are zeroed by k7_reset: no access before it completed
+            asm volatile("griddepcontrol.wait;" ::: "memory");
+            if (j == 0 && ok) {
+                const float v = (float)(s01 + s23);
+                st_relaxed_u64(a.Sx + ent, (1ull << 32) | (unsigned long long)__float_as_uint(v));
+                if (a.S_out) a.S_out[ent] = v;
+            }
+        }
+    }
+    if (tid == 0 && !issued) issue_codes();
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    stamp(2);
+
+    // ---- (2) poll this user's E words, replicate G times (bank-rotated stores)
+    {
+        const unsigned long long* Su = a.Sx + (int64_t)u * E;
+        const int rot = lane * G / 32;
+#pragma unroll 1
+        for (int e0 = 0; e0 < E; e0 += 4 * K7_THREADS) {
+            unsigned long long w[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int e = e0 + q * K7_THREADS + tid;
+                w[q] = e < E ? ld_relaxed_u64(Su + e) : (1ull << 32);
+            }
+#pragma unroll 1
+            for (int q = 0; q < 4; ++q) {
+                const int e = e0 + q * K7_THREADS + tid;
+                unsigned long long wq = w[0];
+                if (q == 1) wq = w[1];
+                if (q == 2) wq = w[2];
+                if (q == 3) wq = w[3];
+                long long spins = 0;
+                (void)spins;
+                while ((wq >> 32) == 0ull) {
+                    __nanosleep(32);
+                    wq = ld_relaxed_u64(Su + e);
+                    PQ_SPIN_CHECK(spins);
+                }
+                if (e < E) {
+                    const float v = __uint_as_float((uint32_t)wq);
+                    if constexpr (G >= 4) {
+                        constexpr int NQ = G / 4;
+                        const float4 v4 = make_float4(v, v, v, v);
+                        float4* dst = reinterpret_cast<float4*>(T + (size_t)e * G);
+#pragma unroll
+                        for (int c = 0; c < NQ; ++c) dst[(c + rot) % NQ] = v4;
+                    } else {
+#pragma unroll
+                        for (int c = 0; c < G; ++c) T[(size_t)e * G + c] = v;
+                    }
+                }
+            }
+        }
+    }
+    stamp(3);
+    __syncthreads();                                   // table ready
+    if (cbytes) mbar_wait(bar, 0);                     // codes resident
+    stamp(4);
+
+    // ---- (3) gather-sum: thread t scores items t + 512 j, JB at a time, split-major;
+    // each item's fp32 score replaces the first 4 code bytes of its row
+    const uint32_t gid0 = a.id_base + (uint32_t)i0;
+    uint64_t km = 0ull;                                // this thread's best key (0: no items)
+    {
+        const char* Tb = reinterpret_cast<const char*>(T + lane % G);
+        auto look = [&](int k, uint32_t w, int s) {
+            const uint32_t g = __byte_perm(w, 0u, 0x4440u | (uint32_t)s);
+            return *reinterpret_cast<const float*>(Tb + (size_t)k * bq * G * 4 + (size_t)g * (G * 4));
+        };
+        int jbst = -1;
+        float best = 0.0f;
+#pragma unroll 1
+        for (int jb = 0; jb * K7_THREADS < nit; jb += JB) {
+            uint32_t cw[JB][NW];
+#pragma unroll
+            for (int q = 0; q < JB; ++q) {
+                const int li = (jb + q) * K7_THREADS + tid;
+                const unsigned char* row = Rg + (size_t)(li < nit ? li : 0) * MP;
+                if constexpr (NW == 1) {
+                    cw[q][0] = *reinterpret_cast<const uint32_t*>(row);
+                } else if constexpr (NW == 2) {
+                    const uint2 t = *reinterpret_cast<const uint2*>(row);
+                    cw[q][0] = t.x; cw[q][1] = t.y;
+                } else {
+                    const uint4 t = *reinterpret_cast<const uint4*>(row);
+                    cw[q][0] = t.x; cw[q][1] = t.y; cw[q][2] = t.z; cw[q][3] = t.w;
+                }
+            }
+            float acc[JB];
+#pragma unroll
+            for (int q = 0; q < JB; ++q) acc[q] = look(0, cw[q][0], 0);
+#pragma unroll
+            for (int k = 1; k < M; ++k)
+#pragma unroll
+                for (int q = 0; q < JB; ++q) acc[q] = acc[q] + look(k, cw[q][k >> 2], k & 3);
+#pragma unroll
+            for (int q = 0; q < JB; ++q) {
+                const int li = (jb + q) * K7_THREADS + tid;
+                if (li < nit) {
+                    const float sc0 = acc[q] + 0.0f;   // R1-R3: +0 canonical
+                    *reinterpret_cast<float*>(Rg + (size_t)li * MP) = sc0;
+                    if (jbst < 0 || sc0 > best) { jbst = li; best = sc0; }   // first max = smallest id
+                }
+            }
+        }
+        if (jbst >= 0) km = make_key(best, gid0 + (uint32_t)jbst);
+    }
+
+    // ---- (4) proved floor, candidates, the chunk's sorted top K
+    uint64_t fl;
+    if (K <= K7_NWARP) {
+        // floor = the K-th largest warp maximum (K distinct items reach it); every
+        // warp sorts the NWARP maxima itself -- one barrier
+        const uint64_t wm = k7_warp_max(km);
+        if (lane == 0) fk[warp] = wm;
+        __syncthreads();                               // also: every warp is done with the codes
+        stamp(5);
+        const uint64_t srt = k7_warp_sort_desc(lane < K7_NWARP ? fk[lane] : 0ull);
+        fl = __shfl_sync(FULL, srt, K - 1);
+        stamp(12);
+    } else {
+        // K > NWARP: the K-th largest of the per-warp top-min(K, 32) thread maxima
+        const int KW = K < 32 ? K : 32;
+        const uint64_t srt = k7_warp_sort_desc(km);
+        if (lane < KW) fk[warp * KW + lane] = srt;
+        __syncthreads();
+        stamp(5);
+        fl = k7_block_kth(fk, K7_NWARP * KW, (uint32_t)K, hist, sc);   // >= K keys (K <= 512)
+    }
+    {
+        const float fs = fl ? key_score(fl) : -INFINITY;
+#pragma unroll 1
+        for (int j = 0; j * K7_THREADS < nit; ++j) {
+            const int li = j * K7_THREADS + tid;
+            bool c = false;
+            uint64_t key = 0ull;
+            if (li < nit) {
+                const float s = *reinterpret_cast<const float*>(Rg + (size_t)li * MP);
+                if (s >= fs) { key = make_key(s, gid0 + (uint32_t)li); c = key >= fl; }
+            }
+            k7_append(c, key, cbuf, &count);
+        }
+    }
+    __syncthreads();
+    stamp(6);
+    {
+        const int n = count;
+        uint64_t* out = a.cand + ((int64_t)u * a.chunks + chunk) * K;
+        k7_topk(cbuf, n, K, fk, &count, hist, sc, out);
+        for (int j = n + tid; j < K; j += K7_THREADS) out[j] = 0ull;   // pad: K-th key 0 = fewer than K
+    }
+    stamp(7);
+
+    // ---- (5) ticket; the last CTA of the user merges.  Every thread's list
+    // writes precede the barrier; thread 0's acq_rel fence makes them visible
+    // at gpu scope before its ticket (and the last CTA's fence orders its reads).
+    __syncthreads();
+    if (tid == 0) {
+        fence_acq_rel_gpu();
+        is_last = atomicAdd(&a.done[u], 1u) == (unsigned)(a.chunks - 1);
+        if (is_last) fence_acq_rel_gpu();
+    }
+    __syncthreads();
+    if (!is_last) return;
+    stamp(8);
+    // Every chunk list is sorted and 0-padded, so list c's first key is the
+    // chunk maximum and its K-th key the chunk K-th (0: fewer than K).  The
+    // user's top K are among the keys >= floor = max(largest chunk K-th key,
+    // K-th largest chunk maximum): either proves K keys >= floor.
+    uint64_t* mk = reinterpret_cast<uint64_t*>(sm_raw);   // T + R: merge scratch
+    uint64_t* mx = fk;                                    // chunk maxima [chunks] (<= 2 * threads)
+    const int n2 = a.chunks * K;
+    const uint64_t* cu = a.cand + (int64_t)u * n2;
+    constexpr int PQ = 4;
+    uint64_t v[PQ];
+    if (tid == 0) { count = 0; floor_key = 0ull; }
+#pragma unroll
+    for (int q = 0; q < PQ; ++q) {
+        const int i = q * K7_THREADS + tid;
+        v[q] = i < n2 ? __ldcg(cu + i) : 0ull;
+    }
+    {
+        uint64_t f = 0ull;
+#pragma unroll 1
+        for (int c = tid; c < a.chunks; c += K7_THREADS) {
+            const int ik = c * K + K - 1;
+            if (ik >= PQ * K7_THREADS) {                // else in registers (below)
+                const uint64_t t = __ldcg(cu + ik);
+                f = t > f ? t : f;
+            }
+            if (c * K >= PQ * K7_THREADS) mx[c] = __ldcg(cu + (int64_t)c * K);
+        }
+#pragma unroll
+        for (int q = 0; q < PQ; ++q) {
+            const int i = q * K7_THREADS + tid;
+            if (i < n2) {
+                const int r = i % K;
+                if (r == K - 1) f = v[q] > f ? v[q] : f;
+                if (r == 0) mx[i / K] = v[q];
+            }
+        }
+        f = k7_warp_max(f);
+        __syncthreads();                               // count / floor_key reset seen; mx complete
+        stamp(13);
+        if (lane == 0 && f) atomicMax(&floor_key, (unsigned long long)f);
+        // the K-th largest chunk maximum: per warp the K largest of its 32, then all
+        const int nwm = (a.chunks + 31) / 32;
+        const int cpad = (a.chunks + 1) & ~1;          // wk 16-byte aligned (k7_rank)
+        if (K <= 32 && nwm * K <= 2 * K7_THREADS - cpad) {
+            uint64_t* wk = mx + cpad;                  // [nwm][K]
+            if (warp < nwm) {
+                const int c = warp * 32 + lane;
+                const uint64_t srt = k7_warp_sort_desc(c < a.chunks ? mx[c] : 0ull);
+                if (lane < K) wk[warp * K + lane] = srt;
+            }
+            __syncthreads();
+            stamp(14);
+            if (warp == 0) {
+                const int nk = nwm * K;
+                uint64_t best = 0ull;
+                for (int i = lane; i < nk; i += 32) {
+                    const uint64_t mine = wk[i];
+                    if (mine && k7_rank(wk, nk, mine) == K - 1) best = mine;
+                }
+                best = k7_warp_max(best);
+                if (lane == 0 && best) atomicMax(&floor_key, (unsigned long long)best);
+            }
+        } else if (a.chunks >= K) {
+            const uint64_t t = k7_block_kth(mx, a.chunks, (uint32_t)K, hist, sc);
+            if (tid == 0 && t) atomicMax(&floor_key, (unsigned long long)t);
+        }
+        __syncthreads();
+    }
+    stamp(9);
+    {
+        const uint64_t fl2 = floor_key;
+#pragma unroll
+        for (int q = 0; q < PQ; ++q) k7_append(v[q] != 0ull && v[q] >= fl2, v[q], mk, &count);
+#pragma unroll 1
+        for (int i0m = PQ * K7_THREADS; i0m < n2; i0m += K7_THREADS) {
+            const int i = i0m + tid;
+            const uint64_t t = i < n2 ? __ldcg(cu + i) : 0ull;
+            k7_append(t != 0ull && t >= fl2, t, mk, &count);
+        }
+    }
+    __syncthreads();
+    stamp(10);
+    {
+        // the sorted top K keys -> fk[K7_THREADS ..] (free now), then ids / scores
+        const int n3 = count;
+        uint64_t* res = fk + K7_THREADS;
+        k7_topk(mk, n3, K, fk, &count, hist, sc, res);
+        __syncthreads();
+        for (int j = tid; j < K; j += K7_THREADS) {
+            const uint64_t key = j < n3 ? res[j] : 0ull;
+            a.ids[(int64_t)u * K + j] = key ? key_id(key) : -1;
+            a.scores[(int64_t)u * K + j] = key ? key_score(key) : -INFINITY;
+        }
+    }
+    stamp(11);
+}
+
+// Zeroes the call's tickets and tagged S words ([bytes] at p, 16-byte multiple);
+// K7 is its programmatic dependent and starts at once.
+__global__ void k7_reset(uint4* p, int n16) {
+    asm volatile("griddepcontrol.launch_dependents;");
+    for (int i = threadIdx.x; i < n16; i += blockDim.x) p[i] = make_uint4(0u, 0u, 0u, 0u);
+}
+
+// ---------------------------------------------------------------- host side
+typedef void (*K7Fn)(const K7Args);
+
+static K7Fn k7_fn(int m, int G) {
+    switch (m) {
+        case 4: return G == 16 ? k7_resident<4, 16> : nullptr;
+        case 8: return G == 16 ? k7_resident<8, 16> : nullptr;
+        case 16: return G == 16 ? k7_resident<16, 16> : (G == 8 ? k7_resident<16, 8> : nullptr);
+        default: return nullptr;
+    }
+}
+static int k7_mp(int m) { return (m + 3) / 4 * 4; }
+static size_t k7_rbytes(int m, int64_t ci) { return align_up((size_t)ci * (size_t)k7_mp(m), 128); }
+// the table region, also the candidate buffer once the chunk is scored (>= 1 key per item)
+static size_t k7_tbytes(int m, int b, int G, int64_t ci) {
+    return std::max(align_up((size_t)m * b * G * 4, 128), (size_t)ci * 8);
+}
+static size_t k7_static_bytes() { return 2 * K7_THREADS * 8 + 256 * 4 + 64 + 64; }
+
+// Workspace: [done B u32 | pad to 256][Sx B*E u64][cand B*chunks*K u64]
+static size_t k7_reset_bytes(int B, int E) { return 256 + align_up((size_t)B * E * 8, 256); }
+
+bool k7_resident_plan(const pq_index_s* idx, int B, int d, int K, K6Plan& p) {
+    const int m = idx->m, b = idx->b;
+    const pq_tuning& t = idx->tuning;
+    if (t.cluster > 0) return false;                   // cluster modes are K6's
+    if (B < 1 || B > 4 || K < 1 || K > K7_MAXK || d % m) return false;
+    if (m != 4 && m != 8 && m != 16) return false;
+    int G = (size_t)m * b * 16 * 4 <= 128 * 1024 ? 16 : 8;
+    if (t.users_per_row > 0) G = std::min(G, pow2_ceil(t.users_per_row));
+    K7Fn fn = k7_fn(m, G);
+    if (!fn) return false;
+    const int64_t N = idx->N;
+    const int cap = idx->num_sms / B;                  // one CTA per SM, one wave
+    if (cap < 1) return false;
+    int64_t ch = std::max<int64_t>(1, std::min<int64_t>(cap, ceil_div(N, 512)));   // >= 512 items per CTA
+    if (t.chunks > 0) ch = std::min<int64_t>(t.chunks, cap);
+    const size_t budget = idx->smem_optin - k7_static_bytes();
+    int64_t ci = 0;
+    size_t smem = 0;
+    for (;; --ch) {                                    // fewer chunks while the merge scratch does not fit
+        ci = (int64_t)align_up((size_t)ceil_div(N, ch), 16);
+        const int64_t che = ceil_div(N, ci);
+        const size_t tr = k7_tbytes(m, b, G, ci) + k7_rbytes(m, ci);
+        smem = std::max(tr, align_up((size_t)che * K * 8, 128));   // T + R: merge scratch
+        if (smem <= budget || ch == 1 || (size_t)che * K * 8 <= tr) break;
+    }
+    ch = ceil_div(N, ci);
+    if (ci > (int64_t)K7_THREADS * K7_JMAX || smem > budget) return false;
+    ensure_max_smem(reinterpret_cast<const void*>(fn), (int)smem);
+    int per_sm = 0;
+    PQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, K7_THREADS, smem));
+    if (per_sm < 1 || (int64_t)per_sm * idx->num_sms < (int64_t)B * ch) return false;
+    p = K6Plan{};
+    p.resident = 1;
+    p.G = G;
+    p.gridsync = 1;
+    p.chunks = (int)ch;
+    p.chunk_items = ci;
+    p.grid = B * (int)ch;
+    p.smem = smem;
+    p.cand_bytes = (size_t)B * ch * K * 8;
+    return true;
+}
+
+size_t k7_resident_ws_bytes(const K6Plan& p, int B, int E) {
+    return k7_reset_bytes(B, E) + align_up(p.cand_bytes, 256);
+}
+
+void launch_k7_resident(const pq_index_s* idx, const K6Plan& p, const float* phi, const float* psi, int B,
+                        int d, int K, void* ws, float* S_out, int32_t* ids, float* scores, cudaStream_t st) {
+    const int E = idx->m * idx->b;
+    K7Args a{};
+    a.codes = idx->d_codes;
+    a.phi = phi; a.psi = psi; a.S_out = S_out;
+    char* w = static_cast<char*>(ws);
+    a.done = reinterpret_cast<unsigned int*>(w);
+    a.Sx = reinterpret_cast<unsigned long long*>(w + 256);
+    const size_t rb = k7_reset_bytes(B, E);
+    a.cand = reinterpret_cast<uint64_t*>(w + rb);
+    a.ids = ids; a.scores = scores;
+    a.N = idx->N;
+    a.mp = idx->lay.mp; a.b = idx->b; a.B = B; a.K = K; a.d = d; a.L = d / idx->m;
+    a.id_base = (uint32_t)idx->id_base;
+    a.chunks = p.chunks;
+    a.chunk_items = (int)p.chunk_items;
+    k7_reset<<<1, 256, 0, st>>>(reinterpret_cast<uint4*>(w), (int)(rb / 16));
+    count_launch();
+    check_launch("k7_reset");
+    cudaLaunchConfig_t cfg{};
+    cudaLaunchAttribute at[2];
+    cfg.gridDim = dim3((unsigned)p.grid);
+    cfg.blockDim = dim3(K7_THREADS);
+    cfg.dynamicSmemBytes = p.smem;
+    cfg.stream = st;
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 2;
+    const char* tf = getenv("PQTOPK_K6_TRACE");
+    if (tf && *tf) {
+        PQ_CUDA(cudaMalloc(&a.trace, (size_t)p.grid * 32 * 8));
+        PQ_CUDA(cudaMemsetAsync(a.trace, 0, (size_t)p.grid * 32 * 8, st));
+    }
+    PQ_CUDA(cudaLaunchKernelEx(&cfg, k7_fn(idx->m, p.G), a));
+    count_launch();
+    check_launch("k7_resident");
+    if (a.trace) {                                     // diagnostics only: per-CTA phase stamps
+        std::vector<long long> h((size_t)p.grid * 32);
+        PQ_CUDA(cudaMemcpyAsync(h.data(), a.trace, h.size() * 8, cudaMemcpyDeviceToHost, st));
+        PQ_CUDA(cudaStreamSynchronize(st));
+        cudaFree(a.trace);
+        if (FILE* f = fopen(tf, "wb")) {
+            const int hdr[2] = {p.grid, 32};
+            fwrite(hdr, sizeof hdr, 1, f);
+            fwrite(h.data(), 8, h.size(), f);
+            fclose(f);
+        }
+    }
+}
+
+}  // namespace pq

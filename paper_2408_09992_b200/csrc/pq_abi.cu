@@ -485,7 +485,7 @@ pq_status pq_score_topk(pq_index idx, const float* S, int32_t B, int32_t K, void
 static bool use_k6(pq_index_s* idx, int B, int d, int K, int flags, K6Plan& p) {
     if (flags & PQ_SEARCH_NO_FUSED) return false;
     const int v = idx->tuning.variant;
-    if (v != 0 && v != 5) return false;
+    if (v != 0 && v != 5 && v != 7) return false;
     return k6_query_plan(idx, B, d, K, p);
 }
 
@@ -582,7 +582,7 @@ pq_status pq_search_plan_info(pq_index idx, int32_t B, int32_t d, int32_t K, int
     need(d >= idx->m && d % idx->m == 0, "d must be a positive multiple of m");
     K6Plan kp;
     if (use_k6(idx, B, d, K, 0, kp)) {
-        out[0] = 5; out[1] = kp.G; out[2] = kp.gridsync ? 0 : kp.CL; out[3] = 8;
+        out[0] = kp.resident ? 7 : 5; out[1] = kp.G; out[2] = kp.gridsync ? 0 : kp.CL; out[3] = 8;
         out[4] = kp.grid; out[5] = kp.chunks; out[6] = 0; out[7] = (int64_t)kp.smem;
     } else {
         K2Plan p = plan_k2(idx, B, K);

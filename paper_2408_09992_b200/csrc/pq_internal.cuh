@@ -159,12 +159,18 @@ struct K2Plan {
 struct K6Plan {
     int G = 0, nst = 0, CL = 0, chunks = 0, grid = 0;
     int gridsync = 0;             // 1: cooperative grid mode (S shared through L2), else clusters of CL
+    int resident = 0;             // 1: K7 (k7_resident.cu): each CTA's code chunk resident in smem
     int64_t chunk_items = 0;
     size_t smem = 0, cand_bytes = 0;
 };
 bool k6_query_plan(pq_index_s* idx, int B, int d, int K, K6Plan& p);   // cached per index
 void k6_cache_free(pq_index_s* idx);
 size_t k6_query_ws_bytes(const K6Plan& p, int B, int E);
+// K7 (k7_resident.cu): the chunk-resident single-launch query kernel (B <= 4, small catalogues)
+bool k7_resident_plan(const pq_index_s* idx, int B, int d, int K, K6Plan& p);
+size_t k7_resident_ws_bytes(const K6Plan& p, int B, int E);
+void launch_k7_resident(const pq_index_s* idx, const K6Plan& p, const float* phi, const float* psi, int B,
+                        int d, int K, void* ws, float* S_out, int32_t* ids, float* scores, cudaStream_t st);
 void launch_k6_query(const pq_index_s* idx, const K6Plan& p, const float* phi, const float* psi, int B,
                      int d, int K, void* ws, float* S_out, int32_t* ids, float* scores, cudaStream_t st);
 // v4 helpers (k2_latency.cu): small batches (B <= 4), lane = item

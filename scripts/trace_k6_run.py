@@ -19,8 +19,10 @@ if tun:
 F = torch.from_numpy(pqsynth.phi(cfg)).cuda()
 P = torch.from_numpy(pqsynth.psi(cfg)).cuda()
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+noflush = os.environ.get("TRACE_NOFLUSH") == "1"    # warm-L2 comparison
 for i in range(6):
-    flush.fill_(1)
+    if not noflush:
+        flush.fill_(1)
     if i == 5:
         os.environ["PQTOPK_K6_TRACE"] = sys.argv[2]
     pq.pq_search(idx, F, P, cfg.K)

@@ -427,6 +427,11 @@ FUSED_CASES = [
     (529, 20_000_003, 8, 256, 64, 1, 10, "uniform"),   # long chunks (thousands of rounds per CTA)
     (530, 500_001, 8, 128, 64, 2, 20, "zipf"),         # b = 128
     (531, 3_000_001, 4, 256, 64, 3, 100, "uniform"),   # m = 4
+    # K7 (chunk-resident codes) shapes
+    (532, 1_700_001, 8, 256, 64, 1, 10, "uniform"),    # near K7's chunk capacity, ragged tail
+    (533, 600_001, 16, 256, 64, 1, 50, "zipf"),        # m = 16: 8 table copies
+    (534, 300_000, 8, 256, 64, 4, 30, "few"),          # 4 users, heavy ties
+    (535, 100_000, 4, 16, 64, 1, 300, "uniform"),      # K = 300 ties: radix-selected floor / cuts
 ]
 
 
@@ -442,9 +447,10 @@ def test_fused_query_parity(pq, torch, orc, case):
     S_ref = pq.pq_subscores(Fd, Pd).cpu().numpy()
     check_S(orc, F, P, S_ref)
     ref = orc.pq_topk(G, S_ref, K, id_base=seed)
-    assert idx.search_plan(B, d, K)["variant"] == 5
+    assert idx.search_plan(B, d, K)["variant"] in (5, 7)
     for tun in (dict(), dict(cluster=1), dict(cluster=2, chunks=6), dict(cluster=8), dict(variant=5, chunks=1),
-                dict(chunks=3), dict(users_per_row=8, chunks=4)):
+                dict(chunks=3), dict(users_per_row=8, chunks=4), dict(variant=5), dict(variant=5, chunks=3),
+                dict(variant=7, chunks=2), dict(variant=7, users_per_row=8)):
         idx.set_tuning(**tun)
         S_out = torch.full((B, m, b), float("nan"), device="cuda")
         i, s = pq.pq_search(idx, Fd, Pd, K, S_out=S_out)
