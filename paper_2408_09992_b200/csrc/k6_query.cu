@@ -842,7 +842,7 @@ bool k6_query_plan(pq_index_s* idx, int B, int d, int K, K6Plan& p) {
         }
     // K7 (codes of each CTA's chunk resident in shared memory) whenever it
     // applies, unless the tuning forces K6 (variant 5); K6 otherwise
-    bool ok = idx->tuning.variant == 7 && k7_resident_plan(idx, B, d, K, p);   // (auto: K6 until K7 is faster)
+    bool ok = idx->tuning.variant != 5 && k7_resident_plan(idx, B, d, K, p);
     if (!ok && idx->tuning.variant != 7) ok = plan_uncached(idx, B, d, K, p);
     v->push_back(K6CacheEnt{B, d, K, idx->tuning, ok, p});
     return ok;

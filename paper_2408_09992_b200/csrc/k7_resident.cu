@@ -64,12 +64,11 @@ constexpr int K7_NWARP = K7_THREADS / 32;
 constexpr int K7_JMAX = 24;        // items per thread
 constexpr int K7_MAXK = 512;
 
-// Helpers are out of line: the chunk phase runs them first, so the last CTA's
-// merge finds their code in the instruction cache (a once-per-launch path is
-// otherwise fetched cold).
+// (Warp-collective helpers stay inline: out of line, every shuffle becomes a
+// divergence-safe WARPSYNC.COLLECTIVE sequence.)
 
 // one key per lane, bitonic across the warp, descending (lane 0 = largest)
-__device__ __noinline__ uint64_t k7_warp_sort_desc(uint64_t v) {
+__device__ __forceinline__ uint64_t k7_warp_sort_desc(uint64_t v) {
     const int lane = threadIdx.x & 31;
 #pragma unroll
     for (int k = 2; k <= 32; k <<= 1)
@@ -90,7 +89,7 @@ __device__ __noinline__ uint64_t k7_block_kth(const uint64_t* buf, int n, uint32
 // Rank of `mine` among buf[0..n) (keys unique; 0 = empty never outranks):
 // the number of keys above it.  Eight independent 128-bit broadcast loads in
 // flight (the loop is load-latency bound otherwise).  buf 16-byte aligned.
-__device__ __noinline__ int k7_rank(const uint64_t* buf, int n, uint64_t mine) {
+__device__ __forceinline__ int k7_rank(const uint64_t* buf, int n, uint64_t mine) {
     int r0 = 0, r1 = 0;
     int j = 0;
     for (; j + 16 <= n; j += 16) {
@@ -129,7 +128,7 @@ __device__ __forceinline__ void k7_append(bool keep, uint64_t key, uint64_t* buf
 // (global memory) for rank < min(K, n).  n <= 32: warp 0 sorts them; n <= 256:
 // ranked all-pairs; larger: radix-select the K-th key, keep the K keys >= it
 // (into tmp, >= K slots) and rank those.  All threads call it.
-__device__ __noinline__ void k7_topk(const uint64_t* buf, int n, int K, uint64_t* tmp, int* count,
+__device__ __forceinline__ void k7_topk(const uint64_t* buf, int n, int K, uint64_t* tmp, int* count,
                                      uint32_t* hist, unsigned long long* sc, uint64_t* out) {
     const int tid = threadIdx.x;
     if (n <= 32) {
@@ -167,7 +166,6 @@ __device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long
 __device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned long long v) {
     asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" :: "l"(p), "l"(v) : "memory");
 }
-__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 
 // Shared memory: [T: M*b*G fp32 | R: codes of the chunk (each row's first 4
 // bytes then hold the item's score), then candidate keys] (dynamic) + fk[1024]
@@ -185,7 +183,7 @@ __global__ void __launch_bounds__(K7_THREADS, 1) k7_resident(const K7Args a) {
     __shared__ unsigned long long floor_key;
     __shared__ int count;
     __shared__ int is_last;
-    __shared__ __align__(8) unsigned long long mbar;
+    __shared__ __align__(8) unsigned long long mbar[K7_JMAX / 8];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int bq = a.b;
     const int E = M * bq;
@@ -200,7 +198,8 @@ __global__ void __launch_bounds__(K7_THREADS, 1) k7_resident(const K7Args a) {
     const int64_t i0 = (int64_t)chunk * a.chunk_items;
     const int nit = (int)max((int64_t)0, min((int64_t)a.chunk_items, a.N - i0));
     const uint32_t cbytes = (uint32_t)align_up((size_t)nit * MP, 16);
-    const uint32_t bar = smem_u32(&mbar);
+    const uint32_t bar0 = smem_u32(mbar);
+    constexpr uint32_t PIECE = 8u * K7_THREADS * MP;   // code bytes of one scoring batch (JB items per thread)
     auto stamp = [&](int i) {                          // diagnostics builds only (-DK6_TRACE)
 #ifdef K6_TRACE
         if (a.trace && tid == 0) {
@@ -213,18 +212,19 @@ __global__ void __launch_bounds__(K7_THREADS, 1) k7_resident(const K7Args a) {
 #endif
     };
     stamp(0);
-    // the chunk's code rows -> R in bulk TMA copies on one mbarrier (no ring: the
-    // whole chunk is resident).  Issued by thread 0 right after its own sub-id
-    // score loads, so the sub-id score requests are not queued behind 10 MB of codes.
+    // the chunk's code rows -> R in bulk TMA copies (no ring: the whole chunk is
+    // resident), one mbarrier per scoring batch so scoring starts on the first
+    // piece.  Issued by thread 0 right after its own sub-id score loads, so the
+    // sub-id score requests are not queued behind the codes.
     auto issue_codes = [&]() {
-        if (cbytes) {
-            mbar_expect_tx(bar, cbytes);
-            for (uint32_t o = 0; o < cbytes; o += 32768u)
-                bulk_g2s(smem_u32(Rg) + o, a.codes + i0 * MP + o, min(32768u, cbytes - o), bar);
+        for (uint32_t o = 0, p = 0; o < cbytes; o += PIECE, ++p) {
+            const uint32_t nb = min(PIECE, cbytes - o);
+            mbar_expect_tx(bar0 + 8u * p, nb);
+            bulk_g2s(smem_u32(Rg) + o, a.codes + i0 * MP + o, nb, bar0 + 8u * p);
         }
     };
     if (tid == 0) {
-        mbar_init(bar, 1);
+        for (int p = 0; p < K7_JMAX / 8; ++p) mbar_init(bar0 + 8u * p, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         count = 0;
         floor_key = 0ull;
@@ -320,7 +320,6 @@ __global__ void __launch_bounds__(K7_THREADS, 1) k7_resident(const K7Args a) {
     }
     stamp(3);
     __syncthreads();                                   // table ready
-    if (cbytes) mbar_wait(bar, 0);                     // codes resident
     stamp(4);
 
     // ---- (3) gather-sum: thread t scores items t + 512 j, JB at a time, split-major;
@@ -337,6 +336,7 @@ __global__ void __launch_bounds__(K7_THREADS, 1) k7_resident(const K7Args a) {
         float best = 0.0f;
 #pragma unroll 1
         for (int jb = 0; jb * K7_THREADS < nit; jb += JB) {
+            mbar_wait(bar0 + 8u * (uint32_t)(jb / JB), 0);   // this batch's code rows resident
             uint32_t cw[JB][NW];
 #pragma unroll
             for (int q = 0; q < JB; ++q) {
@@ -394,17 +394,43 @@ __global__ void __launch_bounds__(K7_THREADS, 1) k7_resident(const K7Args a) {
         fl = k7_block_kth(fk, K7_NWARP * KW, (uint32_t)K, hist, sc);   // >= K keys (K <= 512)
     }
     {
+        // candidates = keys >= fl: count per thread (four loads in flight), one
+        // atomic per warp, write
         const float fs = fl ? key_score(fl) : -INFINITY;
+        auto cand = [&](int li, float s, uint64_t& key) {
+            if (!(s >= fs)) return false;
+            key = make_key(s, gid0 + (uint32_t)li);
+            return key >= fl;
+        };
+        auto score = [&](int li) { return *reinterpret_cast<const float*>(Rg + (size_t)li * MP); };
+        int nc = 0;
+        int li = tid;
 #pragma unroll 1
-        for (int j = 0; j * K7_THREADS < nit; ++j) {
-            const int li = j * K7_THREADS + tid;
-            bool c = false;
-            uint64_t key = 0ull;
-            if (li < nit) {
-                const float s = *reinterpret_cast<const float*>(Rg + (size_t)li * MP);
-                if (s >= fs) { key = make_key(s, gid0 + (uint32_t)li); c = key >= fl; }
+        for (; li + 3 * K7_THREADS < nit; li += 4 * K7_THREADS) {
+            float s4[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) s4[q] = score(li + q * K7_THREADS);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) { uint64_t key; nc += cand(li + q * K7_THREADS, s4[q], key) ? 1 : 0; }
+        }
+#pragma unroll 1
+        for (; li < nit; li += K7_THREADS) { uint64_t key; nc += cand(li, score(li), key) ? 1 : 0; }
+        int incl = nc;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(FULL, incl, o);
+            if (lane >= o) incl += t;
+        }
+        const int tot = __shfl_sync(FULL, incl, 31);
+        int base = 0;
+        if (lane == 31 && tot) base = atomicAdd(&count, tot);
+        base = __shfl_sync(FULL, base, 31) + incl - nc;
+        if (nc) {
+#pragma unroll 1
+            for (int l2 = tid; l2 < nit; l2 += K7_THREADS) {
+                uint64_t key;
+                if (cand(l2, score(l2), key)) cbuf[base++] = key;
             }
-            k7_append(c, key, cbuf, &count);
         }
     }
     __syncthreads();
@@ -418,13 +444,13 @@ __global__ void __launch_bounds__(K7_THREADS, 1) k7_resident(const K7Args a) {
     stamp(7);
 
     // ---- (5) ticket; the last CTA of the user merges.  Every thread's list
-    // writes precede the barrier; thread 0's acq_rel fence makes them visible
-    // at gpu scope before its ticket (and the last CTA's fence orders its reads).
+    // writes precede the barrier; thread 0's acq_rel ticket releases them at gpu
+    // scope (and, in the last CTA, acquires the other CTAs' lists).
     __syncthreads();
     if (tid == 0) {
-        fence_acq_rel_gpu();
-        is_last = atomicAdd(&a.done[u], 1u) == (unsigned)(a.chunks - 1);
-        if (is_last) fence_acq_rel_gpu();
+        unsigned int old;
+        asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(a.done + u) : "memory");
+        is_last = old == (unsigned)(a.chunks - 1);
     }
     __syncthreads();
     if (!is_last) return;
@@ -432,7 +458,7 @@ __global__ void __launch_bounds__(K7_THREADS, 1) k7_resident(const K7Args a) {
     // Every chunk list is sorted and 0-padded, so list c's first key is the
     // chunk maximum and its K-th key the chunk K-th (0: fewer than K).  The
     // user's top K are among the keys >= floor = max(largest chunk K-th key,
-    // K-th largest chunk maximum): either proves K keys >= floor.
+    // largest per-32-chunk K-th chunk maximum): either proves K keys >= floor.
     uint64_t* mk = reinterpret_cast<uint64_t*>(sm_raw);   // T + R: merge scratch
     uint64_t* mx = fk;                                    // chunk maxima [chunks] (<= 2 * threads)
     const int n2 = a.chunks * K;
@@ -469,27 +495,14 @@ __global__ void __launch_bounds__(K7_THREADS, 1) k7_resident(const K7Args a) {
         __syncthreads();                               // count / floor_key reset seen; mx complete
         stamp(13);
         if (lane == 0 && f) atomicMax(&floor_key, (unsigned long long)f);
-        // the K-th largest chunk maximum: per warp the K largest of its 32, then all
-        const int nwm = (a.chunks + 31) / 32;
-        const int cpad = (a.chunks + 1) & ~1;          // wk 16-byte aligned (k7_rank)
-        if (K <= 32 && nwm * K <= 2 * K7_THREADS - cpad) {
-            uint64_t* wk = mx + cpad;                  // [nwm][K]
-            if (warp < nwm) {
-                const int c = warp * 32 + lane;
+        // a floor from the chunk maxima: each warp's K-th largest of its 32 chunk
+        // maxima (K chunks hold a key >= it); the largest over the warps
+        if (K <= 32) {
+            for (int w0 = warp * 32; w0 < a.chunks; w0 += K7_THREADS) {
+                const int c = w0 + lane;
                 const uint64_t srt = k7_warp_sort_desc(c < a.chunks ? mx[c] : 0ull);
-                if (lane < K) wk[warp * K + lane] = srt;
-            }
-            __syncthreads();
-            stamp(14);
-            if (warp == 0) {
-                const int nk = nwm * K;
-                uint64_t best = 0ull;
-                for (int i = lane; i < nk; i += 32) {
-                    const uint64_t mine = wk[i];
-                    if (mine && k7_rank(wk, nk, mine) == K - 1) best = mine;
-                }
-                best = k7_warp_max(best);
-                if (lane == 0 && best) atomicMax(&floor_key, (unsigned long long)best);
+                const uint64_t kk = __shfl_sync(FULL, srt, K - 1);
+                if (lane == 0 && kk) atomicMax(&floor_key, (unsigned long long)kk);
             }
         } else if (a.chunks >= K) {
             const uint64_t t = k7_block_kth(mx, a.chunks, (uint32_t)K, hist, sc);
@@ -526,6 +539,7 @@ __global__ void __launch_bounds__(K7_THREADS, 1) k7_resident(const K7Args a) {
     stamp(11);
 }
 
+
 // Zeroes the call's tickets and tagged S words ([bytes] at p, 16-byte multiple);
 // K7 is its programmatic dependent and starts at once.
 __global__ void k7_reset(uint4* p, int n16) {
@@ -550,7 +564,7 @@ static size_t k7_rbytes(int m, int64_t ci) { return align_up((size_t)ci * (size_
 static size_t k7_tbytes(int m, int b, int G, int64_t ci) {
     return std::max(align_up((size_t)m * b * G * 4, 128), (size_t)ci * 8);
 }
-static size_t k7_static_bytes() { return 2 * K7_THREADS * 8 + 256 * 4 + 64 + 64; }
+static size_t k7_static_bytes() { return 2 * K7_THREADS * 8 + 256 * 4 + 256; }
 
 // Workspace: [done B u32 | pad to 256][Sx B*E u64][cand B*chunks*K u64]
 static size_t k7_reset_bytes(int B, int E) { return 256 + align_up((size_t)B * E * 8, 256); }
@@ -582,6 +596,8 @@ bool k7_resident_plan(const pq_index_s* idx, int B, int d, int K, K6Plan& p) {
     }
     ch = ceil_div(N, ci);
     if (ci > (int64_t)K7_THREADS * K7_JMAX || smem > budget) return false;
+    // auto: tiny catalogues (C1) are faster on K6, whose 256-thread CTAs ramp sooner
+    if (t.variant != 7 && ci < 2048) return false;
     ensure_max_smem(reinterpret_cast<const void*>(fn), (int)smem);
     int per_sm = 0;
     PQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, K7_THREADS, smem));

@@ -7,10 +7,10 @@ raw = open(sys.argv[1], "rb").read()
 grid, n = np.frombuffer(raw[:8], np.int32)
 t = np.frombuffer(raw[8:], np.int64).reshape(grid, n).astype(np.float64)
 t0 = t[:, 0].min()
-names = ["start", "S share computed", "S reset waited", "S polled + table", "codes resident",
-         "scored + warp maxima", "candidates", "chunk list written", "merge: start (last CTA)",
-         "merge: floor", "merge: gathered", "merge: written", "chunk floor sorted",
-         "merge: keys loaded", "merge: maxima sorted"]
+names = ["start", "S share computed", "S reset waited", "S polled + table", "table ready",
+         "scored + warp maxima", "candidates", "chunk published", "merge: start (last CTA)",
+         "merge: floor", "merge: gathered", "merge: written", "chunk floor",
+         "merge: maxima loaded"]
 print(f"grid {grid}; times in us from the first CTA start (min / median / max over CTAs)")
 for i, nm in enumerate(names):
     v = t[:, i][t[:, i] > 0] - t0
