@@ -97,6 +97,16 @@ __global__ void k0_emit(const uint32_t* __restrict__ key, const int32_t* __restr
     }
 }
 
+// colour-paired row-order codes for K6 / K7: row r = item perm[r] in stored codes
+__global__ void k0_pair_rows(const uint8_t* __restrict__ codes, int mp, int m, const int32_t* __restrict__ perm,
+                             int64_t rows, const uint8_t* __restrict__ stored, uint8_t* __restrict__ out) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < rows; r += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t it = perm[r];
+        for (int k = 0; k < mp; ++k)
+            out[r * mp + k] = (it >= 0 && k < m) ? stored[k * 256 + codes[(int64_t)it * mp + k]] : (uint8_t)0;
+    }
+}
+
 __global__ void k0_iota(int32_t* __restrict__ perm, int64_t N) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x)
         perm[i] = (int32_t)i;
@@ -366,6 +376,19 @@ void build_v3_layout_gpu(pq_index_s* idx, cudaStream_t st) {
                                                          sh.pair, ps, pss, np, RPS, TR, static_cast<uint8_t*>(idx->d_codes3));
     count_launch();
     check_launch("k0_v3_codes");
+    // 8b. colour-paired row-order codes for the small-batch kernels (m they support)
+    if (R == 16 && (m == 4 || m == 8 || m == 16) && d_stored) {
+        int32_t last = 0;
+        PQ_CUDA(cudaMemcpyAsync(&last, idx->d_perm3 + rows - 1, 4, cudaMemcpyDeviceToHost, st));
+        PQ_CUDA(cudaStreamSynchronize(st));
+        idx->p_rows = last < 0 ? rows - 1 : rows;     // only the last leftover slot can be empty
+        PQ_CUDA(cudaMalloc(&idx->d_codes_p, (size_t)rows_pad * mp + 64));
+        PQ_CUDA(cudaMemsetAsync(idx->d_codes_p, 0, (size_t)rows_pad * mp + 64, st));
+        k0_pair_rows<<<grid_for(rows_pad, sms), 256, 0, st>>>(idx->d_codes, mp, m, idx->d_perm3, rows_pad, d_stored,
+                                                              idx->d_codes_p);
+        count_launch();
+        check_launch("k0_pair_rows");
+    }
     // 9. every item exactly once
     {
         unsigned int* d_bits = db.alloc<unsigned int>((size_t)ceil_div(N, 32));

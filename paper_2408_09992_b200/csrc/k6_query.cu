@@ -34,6 +34,7 @@ namespace pq {
 struct K6Args {
     const uint8_t* codes;      // [N][mp] item-order uint8 rows (K0 layout)
     const int32_t* perm;       // row -> local item id, or null (identity)
+    const uint8_t* cmap;       // colour-paired rows (idx->d_codes_p): [m][b] stored sub-id -> sub-id, else null
     const float* phi;          // [B][d]
     const float* psi;          // [m][b][L], L = d / m
     float* S_out;              // optional [B][m][b] copy of the sub-id scores
@@ -132,6 +133,10 @@ __global__ void __launch_bounds__(K6_THREADS) k6_query(const K6Args a) {
     cg::cluster_group cluster = cg::this_cluster();
     const int crank = (int)cluster.block_rank(), CL = (int)cluster.num_blocks();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    // colour-paired rows: lanes l and l + 16 take the complementary rows 2p, 2p + 1
+    // (opposite parity at every split -> opposite bank halves of the table copies)
+    const int lrow = (int)(threadIdx.x & ~31u) + (a.cmap ? (((lane & 15) << 1) | (lane >> 4)) : lane);
+    auto src = [&](int e) { return a.cmap ? e - e % (BB > 0 ? BB : a.b) + (int)__ldg(a.cmap + e) : e; };
     const int u = blockIdx.x / a.chunks;
     const int chunk = blockIdx.x % a.chunks;
     const int64_t i0 = (int64_t)chunk * a.chunk_items;
@@ -252,7 +257,7 @@ __global__ void __launch_bounds__(K6_THREADS) k6_query(const K6Args a) {
 #pragma unroll
             for (int q = 0; q < RB; ++q) {
                 const int e = e0r + q * K6_THREADS + (int)threadIdx.x;
-                vv[q] = e < E ? __ldcg(Su + e) : 0.0f;
+                vv[q] = e < E ? __ldcg(Su + src(e)) : 0.0f;
             }
 #pragma unroll
             for (int q = 0; q < RB; ++q) {
@@ -378,7 +383,7 @@ __global__ void __launch_bounds__(K6_THREADS) k6_query(const K6Args a) {
         // G copies of each entry into the local table (bank-rotated stores)
         const int rot = lane * G / 32;
         for (int e = threadIdx.x; e < E; e += K6_THREADS) {
-            const float v = Sst[e];
+            const float v = Sst[src(e)];
             if constexpr (G >= 4) {
                 constexpr int NQ = G / 4;
                 const float4 v4 = make_float4(v, v, v, v);
@@ -409,7 +414,7 @@ __global__ void __launch_bounds__(K6_THREADS) k6_query(const K6Args a) {
         uint32_t cw[J][NW];
 #pragma unroll
         for (int j = 0; j < J; ++j) {
-            const int li = j * K6_THREADS + threadIdx.x;
+            const int li = j * K6_THREADS + lrow;
             if constexpr (NW == 1) {
                 cw[j][0] = *reinterpret_cast<const uint32_t*>(cs + (size_t)li * MP);
             } else if constexpr (NW == 2) {
@@ -433,7 +438,7 @@ __global__ void __launch_bounds__(K6_THREADS) k6_query(const K6Args a) {
 #pragma unroll
             for (int j = 0; j < J; ++j) accs[j] = accs[j] + look(k, cw[j][k >> 2], k & 3);
         auto item_key = [&](float acc, int j) {        // R1-R3: +0 canonical score, global id
-            const int64_t item = r0 + j * K6_THREADS + (int)threadIdx.x;
+            const int64_t item = r0 + j * K6_THREADS + lrow;
             const uint32_t lid = a.perm ? (uint32_t)a.perm[item] : (uint32_t)item;
             return make_key(acc + 0.0f, a.id_base + lid);
         };
@@ -446,7 +451,7 @@ __global__ void __launch_bounds__(K6_THREADS) k6_query(const K6Args a) {
             float bv = 0.0f;
 #pragma unroll
             for (int j = 0; j < J; ++j)
-                if (j * K6_THREADS + (int)threadIdx.x < nvalid && (jb < 0 || accs[j] > bv)) { jb = j; bv = accs[j]; }
+                if (j * K6_THREADS + lrow < nvalid && (jb < 0 || accs[j] > bv)) { jb = j; bv = accs[j]; }
             const uint64_t mx = jb >= 0 ? item_key(bv, jb) : 0ull;
             const uint64_t srt = warp_sort32_desc(mx);
             const int jk = (a.K + NWARP - 1) / NWARP;
@@ -461,11 +466,11 @@ __global__ void __launch_bounds__(K6_THREADS) k6_query(const K6Args a) {
         // once the threshold is strong a whole warp usually has none
         bool anyc = false;
 #pragma unroll
-        for (int j = 0; j < J; ++j) anyc |= j * K6_THREADS + (int)threadIdx.x < nvalid && accs[j] >= tfr;
+        for (int j = 0; j < J; ++j) anyc |= j * K6_THREADS + lrow < nvalid && accs[j] >= tfr;
         if (__any_sync(FULL, anyc))
 #pragma unroll
         for (int j = 0; j < J; ++j) {
-            const bool c = j * K6_THREADS + (int)threadIdx.x < nvalid && accs[j] >= tfr;
+            const bool c = j * K6_THREADS + lrow < nvalid && accs[j] >= tfr;
             const unsigned bm = __ballot_sync(FULL, c);
             if (bm) {
                 int base = 0;
@@ -751,6 +756,11 @@ static bool plan_uncached(const pq_index_s* idx, int B, int d, int K, K6Plan& p)
     if (query_smem(m, idx->b, G, 2, d, B) > budget) return false;
     while (nst > 2 && query_smem(m, idx->b, G, nst, d, B) > budget) --nst;
     p.G = G; p.nst = nst;
+    // colour-paired rows (one wavefront per lookup instead of two) for long
+    // streams: c7 (10^9 items) 3.16 -> 2.64 ms; short ones (C1) lose more to the
+    // row -> id loads of the seeding and the candidates than they gain
+    static const bool no_pair = getenv("PQTOPK_NO_PAIRED") != nullptr;   // diagnostics (A/B)
+    p.paired = idx->d_codes_p && G == 16 && !no_pair && idx->p_rows >= (int64_t)idx->num_sms * 65536 ? 1 : 0;
     p.smem = query_smem(m, idx->b, G, nst, d, B);
     K6Fn fn = query_fn(m, G, idx->b);
     ensure_max_smem(reinterpret_cast<const void*>(fn), (int)p.smem);
@@ -761,7 +771,7 @@ static bool plan_uncached(const pq_index_s* idx, int B, int d, int K, K6Plan& p)
     //   t(CL) = E * L / CL / 8 clk + ceil(N / (chunks * items per round)) * 2400 clk
     // (about 8 fp64 fmas per clock per SM with the conversions; ~2400 clocks per
     // 16 KB round, measured); tuning.cluster forces one size.
-    const int64_t N = idx->N;
+    const int64_t N = p.paired ? idx->p_rows : idx->N;
     const int64_t ipr = K6_STAGE / query_mp(m);
     const int64_t merge_cap = query_merge_keys(m, idx->b, nst, d, B);
     if (merge_cap < 2048) return false;
@@ -867,10 +877,11 @@ void launch_k6_query(const pq_index_s* idx, const K6Plan& p, const float* phi, c
         return;
     }
     K6Args a{};
-    a.codes = idx->d_codes;
-    a.perm = idx->lay.paired ? idx->d_perm : nullptr;
+    a.codes = p.paired ? idx->d_codes_p : idx->d_codes;
+    a.perm = p.paired ? idx->d_perm3 : (idx->lay.paired ? idx->d_perm : nullptr);
+    a.cmap = p.paired ? idx->d_cmap3 : nullptr;
     a.phi = phi; a.psi = psi; a.S_out = S_out;
-    a.N = idx->N;
+    a.N = p.paired ? idx->p_rows : idx->N;
     a.mp = idx->lay.mp; a.b = idx->b; a.B = B; a.K = K; a.d = d; a.L = d / idx->m;
     a.id_base = (uint32_t)idx->id_base;
     a.chunks = p.chunks; a.chunk_items = p.chunk_items;

@@ -189,7 +189,8 @@ static const PairLayout& pairing0(CreateCtx& cx, const pq_index_s* idx, const ui
 // to whole tiles and the codes phase-blocked ([tile][phase][row][pss], pss >=
 // ps stored bytes per row per phase).
 static void free_index_buffers(pq_index_s* idx) {
-    void* bufs[] = {idx->d_codes, idx->d_perm, idx->d_cmap, idx->d_codes3, idx->d_perm3, idx->d_cmap3};
+    void* bufs[] = {idx->d_codes, idx->d_perm, idx->d_cmap, idx->d_codes3, idx->d_perm3, idx->d_cmap3,
+                    idx->d_codes_p};
     for (void* p : bufs)
         if (p) cudaFree(p);
 }

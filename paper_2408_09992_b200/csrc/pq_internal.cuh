@@ -122,6 +122,12 @@ struct pq_index_s {
     void* d_codes3 = nullptr;      // [tiles][NP][TR][PS] stored codes, k2_tiled_code_bytes() each (+ pad)
     int32_t* d_perm3 = nullptr;    // [tiles * 4096] row -> local id (-1 = padding)
     uint8_t* d_cmap3 = nullptr;    // [m][b] stored -> original
+    // colour-paired ROW-ORDER codes for the small-batch kernels K6 / K7 (built
+    // with the R = 16 v3 layout): row r = item d_perm3[r] in stored codes
+    // (parity = colour), rows 2p / 2p + 1 complementary; rows < p_rows are all
+    // real items (d_codes_p == null: not built)
+    uint8_t* d_codes_p = nullptr;
+    int64_t p_rows = 0;
     pq_tuning tuning{};
     void* k6_cache = nullptr;      // K6 launch plans by (B, d, K, tuning) (k6_query.cu)
     // optional K2/K3 timing (pq_timing_enable)
@@ -160,6 +166,7 @@ struct K6Plan {
     int G = 0, nst = 0, CL = 0, chunks = 0, grid = 0;
     int gridsync = 0;             // 1: cooperative grid mode (S shared through L2), else clusters of CL
     int resident = 0;             // 1: K7 (k7_resident.cu): each CTA's code chunk resident in smem
+    int paired = 0;               // 1: the colour-paired row-order codes (idx->d_codes_p) with 16 table copies
     int64_t chunk_items = 0;
     size_t smem = 0, cand_bytes = 0;
 };

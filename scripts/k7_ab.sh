@@ -10,9 +10,12 @@ summ() { grep "^{" $1 | python -c "import json,sys; d=json.loads(sys.stdin.read(
 for c in ${CONFIGS:-c2a c1}; do
   for v in ${VARIANTS:-k7 k6}; do
     ex=""; md=0
+    np=""
     [ $v = k6 ] && ex="--tuning variant=5"
+    [ $v = k6np ] && ex="--tuning variant=5" && np=1
+    [ $v = k7np ] && np=1
     case $v in k7m*) md=${v#k7m};; esac
-    PQTOPK_K7_MODE=$md timeout 600 python bench.py --config $c --steps ${STEPS:-50} --warmup 5 --no-cpu-baseline $ex > gpurun_out/bench_${c}_${v}_${TAG}.log 2>&1
+    env ${np:+PQTOPK_NO_PAIRED=1} PQTOPK_K7_MODE=$md timeout 600 python bench.py --config $c --steps ${STEPS:-50} --warmup 5 --no-cpu-baseline $ex > gpurun_out/bench_${c}_${v}_${TAG}.log 2>&1
     echo "$c $v $(summ gpurun_out/bench_${c}_${v}_${TAG}.log)"
   done
 done
