@@ -42,10 +42,7 @@
 namespace pq {
 
 struct K7Args {
-    const uint8_t* codes;          // [N][mp] item-order rows (K0 layout, >= 16 bytes of tail pad), or the
-                                   // colour-paired rows (idx->d_codes_p; N = p_rows) when rowid != null
-    const int32_t* rowid;          // paired rows: row -> local item id; null: row = item
-    const uint8_t* cmap;           // paired rows: [m][b] stored sub-id -> sub-id; null: identity
+    const uint8_t* codes;          // [N][mp] item-order rows (K0 layout, >= 16 bytes of tail pad)
     const float* phi;              // [B][d]
     const float* psi;              // [m][b][L], L = d / m
     float* S_out;                  // optional [B][m][b] copy of the sub-id scores
@@ -284,14 +281,12 @@ __global__ void __launch_bounds__(K7_THREADS, 1) k7_resident(const K7Args a) {
         const unsigned long long* Su = a.Sx + (int64_t)u * E;
         const int rot = lane * G / 32;
 #pragma unroll 1
-        // table entry e = (k, stored g) <- S[k][cmap[k][g]] (paired rows) or S[e]
-        auto src = [&](int e) { return a.cmap ? e - e % bq + (int)__ldg(a.cmap + e) : e; };
         for (int e0 = 0; e0 < E; e0 += 4 * K7_THREADS) {
             unsigned long long w[4];
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
                 const int e = e0 + q * K7_THREADS + tid;
-                w[q] = e < E ? ld_relaxed_u64(Su + src(e)) : (1ull << 32);
+                w[q] = e < E ? ld_relaxed_u64(Su + e) : (1ull << 32);
             }
 #pragma unroll 1
             for (int q = 0; q < 4; ++q) {
@@ -304,7 +299,7 @@ __global__ void __launch_bounds__(K7_THREADS, 1) k7_resident(const K7Args a) {
                 (void)spins;
                 while ((wq >> 32) == 0ull) {
                     __nanosleep(32);
-                    wq = ld_relaxed_u64(Su + src(e));
+                    wq = ld_relaxed_u64(Su + e);
                     PQ_SPIN_CHECK(spins);
                 }
                 if (e < E) {
@@ -327,16 +322,13 @@ __global__ void __launch_bounds__(K7_THREADS, 1) k7_resident(const K7Args a) {
     __syncthreads();                                   // table ready
     stamp(4);
 
-    // ---- (3) gather-sum: thread t scores rows t + 512 j, JB at a time, split-major;
-    // each row's fp32 score replaces its first 4 code bytes.  Paired rows: lanes
-    // l and l + 16 take the two rows of a complementary pair (2p, 2p + 1), whose
-    // stored sub-ids have opposite parity at every split -> opposite bank halves
-    // of the 16-copy table, one wavefront per lookup instead of two.
+    // ---- (3) gather-sum: thread t scores items t + 512 j, JB at a time, split-major;
+    // each item's fp32 score replaces the first 4 code bytes of its row.  (Colour-
+    // paired rows, K6's layout for long streams, were slower here: each CTA's best
+    // key and every candidate then need a row -> id load from cold HBM.)
     const uint32_t gid0 = a.id_base + (uint32_t)i0;
-    auto gid = [&](int row) {                          // global id of the chunk's row
-        return a.rowid ? a.id_base + (uint32_t)__ldg(a.rowid + i0 + row) : gid0 + (uint32_t)row;
-    };
-    const int lrow = (tid & ~31) + (a.rowid ? (((lane & 15) << 1) | (lane >> 4)) : lane);
+    auto gid = [&](int li) { return gid0 + (uint32_t)li; };
+    const int lrow = tid;
     uint64_t km = 0ull;                                // this thread's best key (0: no items)
     {
         const char* Tb = reinterpret_cast<const char*>(T + lane % G);
@@ -377,9 +369,7 @@ __global__ void __launch_bounds__(K7_THREADS, 1) k7_resident(const K7Args a) {
                 if (li < nit) {
                     const float sc0 = acc[q] + 0.0f;   // R1-R3: +0 canonical
                     *reinterpret_cast<float*>(Rg + (size_t)li * MP) = sc0;
-                    // (item order: the first max has the smallest id; paired rows: any of
-                    // the tied maxima -- its key is a real item's key, all the floor needs)
-                    if (jbst < 0 || sc0 > best) { jbst = li; best = sc0; }
+                    if (jbst < 0 || sc0 > best) { jbst = li; best = sc0; }   // first max = smallest id
                 }
             }
         }
@@ -593,12 +583,7 @@ bool k7_resident_plan(const pq_index_s* idx, int B, int d, int K, K6Plan& p) {
     if (t.users_per_row > 0) G = std::min(G, pow2_ceil(t.users_per_row));
     K7Fn fn = k7_fn(m, G);
     if (!fn) return false;
-    // colour-paired rows (conflict-free lookups) only when forced (PQTOPK_K7_PAIRED):
-    // measured slower at C2a (24.6 -> 28.7 us) -- each CTA's best key and every
-    // candidate then needs a row -> id load from cold HBM on the critical path
-    static const bool want_pair = getenv("PQTOPK_K7_PAIRED") != nullptr;
-    const bool paired = idx->d_codes_p && G == 16 && want_pair;
-    const int64_t N = paired ? idx->p_rows : idx->N;
+    const int64_t N = idx->N;
     const int cap = idx->num_sms / B;                  // one CTA per SM, one wave
     if (cap < 1) return false;
     int64_t ch = std::max<int64_t>(1, std::min<int64_t>(cap, ceil_div(N, 512)));   // >= 512 items per CTA
@@ -623,7 +608,6 @@ bool k7_resident_plan(const pq_index_s* idx, int B, int d, int K, K6Plan& p) {
     if (per_sm < 1 || (int64_t)per_sm * idx->num_sms < (int64_t)B * ch) return false;
     p = K6Plan{};
     p.resident = 1;
-    p.paired = paired ? 1 : 0;
     p.G = G;
     p.gridsync = 1;
     p.chunks = (int)ch;
@@ -642,9 +626,7 @@ void launch_k7_resident(const pq_index_s* idx, const K6Plan& p, const float* phi
                         int d, int K, void* ws, float* S_out, int32_t* ids, float* scores, cudaStream_t st) {
     const int E = idx->m * idx->b;
     K7Args a{};
-    a.codes = p.paired ? idx->d_codes_p : idx->d_codes;
-    a.rowid = p.paired ? idx->d_perm3 : nullptr;
-    a.cmap = p.paired ? idx->d_cmap3 : nullptr;
+    a.codes = idx->d_codes;
     a.phi = phi; a.psi = psi; a.S_out = S_out;
     char* w = static_cast<char*>(ws);
     a.done = reinterpret_cast<unsigned int*>(w);
@@ -652,7 +634,7 @@ void launch_k7_resident(const pq_index_s* idx, const K6Plan& p, const float* phi
     const size_t rb = k7_reset_bytes(B, E);
     a.cand = reinterpret_cast<uint64_t*>(w + rb);
     a.ids = ids; a.scores = scores;
-    a.N = p.paired ? idx->p_rows : idx->N;
+    a.N = idx->N;
     a.mp = idx->lay.mp; a.b = idx->b; a.B = B; a.K = K; a.d = d; a.L = d / idx->m;
     a.id_base = (uint32_t)idx->id_base;
     a.chunks = p.chunks;

@@ -432,6 +432,7 @@ FUSED_CASES = [
     (533, 600_001, 16, 256, 64, 1, 50, "zipf"),        # m = 16: 8 table copies
     (534, 300_000, 8, 256, 64, 4, 30, "few"),          # 4 users, heavy ties
     (535, 100_000, 4, 16, 64, 1, 300, "uniform"),      # K = 300 ties: radix-selected floor / cuts
+    (536, 10_000_019, 8, 256, 64, 2, 50, "zipf"),      # K6 on colour-paired rows (long stream), skewed codes
 ]
 
 
