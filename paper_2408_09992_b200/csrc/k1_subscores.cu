@@ -25,6 +25,7 @@
 #include <cstdlib>
 
 #include "pq_internal.cuh"
+#include "ptx_dev.cuh"
 
 namespace pq {
 
@@ -41,6 +42,8 @@ __global__ void __launch_bounds__(K1_THREADS)
 k1_subscores(const float* __restrict__ phi, const float* __restrict__ psi, int B, int d,
              int m, int b, float* __restrict__ S, int gchunk) {
     extern __shared__ double k1_sm[];
+    pdl_wait();                                     // phi / psi may come from the stream predecessor
+    pdl_trigger();                                  // the next kernel (tiled tables) may be scheduled
     double* ps = k1_sm;                             // [gchunk][K1_PS]
     double* fs = k1_sm + (size_t)gchunk * K1_PS;    // [K1_UB][K1_TT]
     const int k = blockIdx.x;
@@ -138,7 +141,7 @@ static void launch_k1(const float* phi, const float* psi, int B, int d, int m, i
     ensure_max_smem(reinterpret_cast<const void*>(k1_subscores<UB>),
                     (int)((std::min(256, K1_MAXOUT / UB) * K1_PS + UB * K1_TT) * sizeof(double)));
     dim3 grid(m, (unsigned)ceil_div(B, UB), (unsigned)ceil_div(b, gchunk));
-    k1_subscores<UB><<<grid, K1_THREADS, smem, st>>>(phi, psi, B, d, m, b, S, gchunk);
+    launch_pdl(k1_subscores<UB>, grid, dim3(K1_THREADS), smem, st, phi, psi, B, d, m, b, S, gchunk);
     count_launch();
     check_launch("k1_subscores");
 }

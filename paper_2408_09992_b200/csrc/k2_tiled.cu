@@ -428,6 +428,10 @@ __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
         tm_fence_after();
         tmem_base = *reinterpret_cast<volatile uint32_t*>(tmem_slot);
     }
+    // everything above overlapped the predecessor (PDL); the tables, thresholds
+    // and buffers below are written by it or by earlier calls
+    pdl_wait();
+    pdl_trigger();                                     // K3 may be scheduled (it waits for this grid)
     // first loads: the unit's phase-0 table and ring positions 0, 1
     if (threadIdx.x == 0 && (int64_t)blockIdx.x < units) {
         if constexpr (NP == 1) {
@@ -820,7 +824,11 @@ __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
 // interleaved table layout (colour-renumbered for R = 16), so K2 can stage a
 // phase's tables with one contiguous bulk copy.
 __global__ void k2_tile_S(const float* __restrict__ S, const uint8_t* __restrict__ cmap, int B, int m,
-                          int b, int R, int n_groups, float* __restrict__ St) {
+                          int b, int R, int n_groups, float* __restrict__ St, unsigned long long* gtau) {
+    pdl_wait();                                        // S comes from K1
+    pdl_trigger();
+    for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < n_groups * R; x += gridDim.x * blockDim.x)
+        gtau[x] = 0ull;                                // the call's shared thresholds start unset
     const int64_t total = (int64_t)n_groups * m * b * R;
     for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < total;
          x += (int64_t)gridDim.x * blockDim.x) {
@@ -841,7 +849,11 @@ __global__ void k2_tile_S(const float* __restrict__ S, const uint8_t* __restrict
 // (the first partial sum of Eq. 5 in the sequential order), then 16 rows per
 // remaining split k = 2 .. m-1.
 __global__ void k2_tile_S_pair(const float* __restrict__ S, int B, int m, int R, int n_groups,
-                               float* __restrict__ St) {
+                               float* __restrict__ St, unsigned long long* gtau) {
+    pdl_wait();                                        // S comes from K1
+    pdl_trigger();
+    for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < n_groups * R; x += gridDim.x * blockDim.x)
+        gtau[x] = 0ull;                                // the call's shared thresholds start unset
     const int rows = 256 + (m - 2) * 16;
     const int64_t total = (int64_t)n_groups * rows * R;
     for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < total;
@@ -998,14 +1010,15 @@ static unsigned long long* gtau_of(const pq_index_s* idx, const K2Plan& p, const
 
 void launch_k2_tiled_prep(const pq_index_s* idx, const K2Plan& p, const float* S, int B, float* St,
                           cudaStream_t st) {
-    PQ_CUDA(cudaMemsetAsync(gtau_of(idx, p, St), 0, (size_t)p.n_groups * p.G * 8, st));
     const TiledShape sh = k2_tiled_shape(idx->m, idx->b);
     const int64_t total = (int64_t)(st_table_bytes(sh, p.n_groups) / 4);
     if (total >= ((int64_t)1 << 32)) fail(PQ_ERR_UNSUPPORTED, "tiled tables exceed 2^32 entries (batch too large)");
     const int threads = 256;
     const int blocks = (int)std::min<int64_t>(ceil_div(total, threads), (int64_t)idx->num_sms * 16);
-    if (sh.pair) k2_tile_S_pair<<<blocks, threads, 0, st>>>(S, B, idx->m, p.G, p.n_groups, St);
-    else k2_tile_S<<<blocks, threads, 0, st>>>(S, idx->d_cmap3, B, idx->m, idx->b, p.G, p.n_groups, St);
+    unsigned long long* gtau = gtau_of(idx, p, St);
+    if (sh.pair) launch_pdl(k2_tile_S_pair, dim3(blocks), dim3(threads), 0, st, S, B, idx->m, p.G, p.n_groups, St, gtau);
+    else launch_pdl(k2_tile_S, dim3(blocks), dim3(threads), 0, st, S, (const uint8_t*)idx->d_cmap3, B, idx->m, idx->b, p.G,
+                    p.n_groups, St, gtau);
     count_launch();
     check_launch("k2_tile_S");
 }
@@ -1047,7 +1060,7 @@ void launch_k2_tiled(const pq_index_s* idx, const K2Plan& p, int B, int K,
         PQ_CUDA(cudaMemsetAsync(a.trace, 0, tn * 8, st));
     }
     K2TFn fn = tiled_fn_shape(k2_tiled_shape(idx->m, idx->b), p.W);
-    fn<<<p.grid, p.W * 32, p.smem, st>>>(a);
+    launch_pdl(fn, dim3(p.grid), dim3(p.W * 32), p.smem, st, a);   // after k2_tile_S (PDL)
     count_launch();
     check_launch("k2_tiled");
     if (a.dbg) {

@@ -8,6 +8,7 @@
 // Keys are unique (score bits + id), so the selected set — and hence the
 // output — is unique: any segmentation / level structure gives the same bits.
 #include "select_dev.cuh"
+#include "ptx_dev.cuh"
 
 namespace pq {
 
@@ -50,6 +51,8 @@ k3_select(Src src, int64_t L, int K, int Kp, uint64_t* __restrict__ out_keys,
           int64_t out_lists, int64_t list_off, int32_t* __restrict__ out_ids,
           float* __restrict__ out_sc) {
     extern __shared__ uint64_t smk[];
+    pdl_wait();                                   // the keys come from the predecessor (PDL launch)
+    pdl_trigger();
     const int u = blockIdx.x;
     const int s = blockIdx.y;
     const int64_t e0 = (int64_t)s * K3_SEG;
@@ -153,8 +156,8 @@ static void launch_k3(Src src, int64_t L, int B, int K, uint64_t* out_keys, int6
     int n_sub = (int)ceil_div(L, K3_SEG);
     dim3 grid((unsigned)B, (unsigned)n_sub);
     int Kp = pow2_ceil(std::min(K, K3_SEG));
-    k3_select<Src><<<grid, K3_THREADS, smem, st>>>(src, L, K, Kp, out_keys, out_lists, list_off,
-                                                   ids, sc);
+    launch_pdl(k3_select<Src>, grid, dim3(K3_THREADS), smem, st, src, L, K, Kp, out_keys, out_lists, list_off,
+               ids, sc);
     count_launch();
     check_launch("k3_select");
 }

@@ -442,6 +442,13 @@ __global__ void __launch_bounds__(K6_THREADS) k6_query(const K6Args a) {
             const uint32_t lid = a.perm ? (uint32_t)a.perm[item] : (uint32_t)item;
             return make_key(acc + 0.0f, a.id_base + lid);
         };
+        // items past the chunk's end (last round only) score NaN: no comparison
+        // passes and fmaxf skips them, so the hot path needs no per-item range checks
+        if (nvalid < IPR) {
+#pragma unroll
+            for (int j = 0; j < J; ++j)
+                if (j * K6_THREADS + lrow >= (int)nvalid) accs[j] = __int_as_float(0x7fffffff);
+        }
         float tfr = tf;
         if (r == 0 && a.K <= NWARP * 32) {
             // threshold seeding: warp w's jk-th largest lane maximum (jk = ceil(K / NWARP))
@@ -451,7 +458,7 @@ __global__ void __launch_bounds__(K6_THREADS) k6_query(const K6Args a) {
             float bv = 0.0f;
 #pragma unroll
             for (int j = 0; j < J; ++j)
-                if (j * K6_THREADS + lrow < nvalid && (jb < 0 || accs[j] > bv)) { jb = j; bv = accs[j]; }
+                if (accs[j] == accs[j] && (jb < 0 || accs[j] > bv)) { jb = j; bv = accs[j]; }   // (NaN: no item)
             const uint64_t mx = jb >= 0 ? item_key(bv, jb) : 0ull;
             const uint64_t srt = warp_sort32_desc(mx);
             const int jk = (a.K + NWARP - 1) / NWARP;
@@ -464,13 +471,13 @@ __global__ void __launch_bounds__(K6_THREADS) k6_query(const K6Args a) {
         }
         // candidates: score >= the proved threshold score (keys only for those);
         // once the threshold is strong a whole warp usually has none
-        bool anyc = false;
+        float amx = accs[0];
 #pragma unroll
-        for (int j = 0; j < J; ++j) anyc |= j * K6_THREADS + lrow < nvalid && accs[j] >= tfr;
-        if (__any_sync(FULL, anyc))
+        for (int j = 1; j < J; ++j) amx = fmaxf(amx, accs[j]);
+        if (__any_sync(FULL, amx >= tfr))
 #pragma unroll
         for (int j = 0; j < J; ++j) {
-            const bool c = j * K6_THREADS + lrow < nvalid && accs[j] >= tfr;
+            const bool c = accs[j] >= tfr;
             const unsigned bm = __ballot_sync(FULL, c);
             if (bm) {
                 int base = 0;

@@ -35,6 +35,23 @@ inline void count_launch(int n = 1) { g_launches.fetch_add(n, std::memory_order_
 
 #define PQ_CUDA(x) ::pq::check_cuda((x), #x)
 
+// Launch with programmatic stream serialization (PDL): only for kernels that
+// call pdl_wait() (ptx_dev.cuh) before touching memory a predecessor writes.
+template <typename... KArgs, typename... Args>
+void launch_pdl(void (*fn)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    check_cuda(cudaLaunchKernelEx(&cfg, fn, static_cast<KArgs>(args)...), "cudaLaunchKernelEx (PDL)");
+}
+
 // ----------------------------------------------------------------------------
 // Checked builds (python -m paper_2408_09992_b200.build --checked ->
 // libpqtopk_checked.so, -DPQTOPK_CHECKED): device-side bounds / invariant

@@ -12,7 +12,7 @@ import paper_2408_09992_b200 as pq  # noqa: E402
 import pqsynth  # noqa: E402
 
 cfg = pqsynth.CONFIGS[sys.argv[1]]
-idx = pq.pq_create(pqsynth.codes(cfg), b=cfg.b, small_batch_only=True)
+idx = pq.pq_create(pqsynth.codes(cfg), b=cfg.b)
 tun = os.environ.get("PQTOPK_TUNING", "")
 if tun:
     idx.set_tuning(**{k: int(v) for k, v in (kv.split("=") for kv in tun.split(",") if kv)})
