@@ -130,6 +130,125 @@ k1_subscores(const float* __restrict__ phi, const float* __restrict__ psi, int B
     }
 }
 
+// Register-blocked variant (UB >= 16 users per block, d/m % 4 == 0): thread
+// (gp, uq) computes the 4 x 2 outputs (users 4 uq .. 4 uq + 3, sub-ids 2 gp,
+// 2 gp + 1), each as four fp64 chains over t = j (mod 4) in ascending t --
+// exactly K1's order (R5b), so S is bit-identical to the plain kernel's.  The
+// tiles are staged transposed ([t][g] and [t][u], fp64), so one t costs one
+// 128-bit psi load and two broadcast 128-bit phi loads for 8 fmas (the plain
+// kernel: two 64-bit loads per fma; it was shared-memory bound).
+constexpr int K1_BTT = 64;    // t-tile of the blocked kernel (one stage for d/m <= 64)
+
+template <int K1_UB>
+__global__ void __launch_bounds__(K1_THREADS)
+k1_blocked(const float* __restrict__ phi, const float* __restrict__ psi, int B, int d,
+           int m, int b, float* __restrict__ S) {
+    constexpr int GCH = K1_MAXOUT / K1_UB;          // sub-ids per block (2 per thread column)
+    constexpr int NGP = GCH / 2;
+    extern __shared__ double k1_sm[];
+    pdl_wait();                                     // phi / psi may come from the stream predecessor
+    pdl_trigger();
+    double* psT = k1_sm;                            // [K1_BTT][GCH]
+    double* phT = k1_sm + (size_t)K1_BTT * GCH;     // [K1_BTT][K1_UB]
+    const int k = blockIdx.x;
+    const int u0 = blockIdx.y * K1_UB;
+    const int nu = min(K1_UB, B - u0);
+    const int dm = d / m;
+    const int g0 = blockIdx.z * GCH;
+    const int nb = min(GCH, b - g0);
+    const int gp = threadIdx.x % NGP, uq = threadIdx.x / NGP;   // uq < K1_UB / 4
+    double acc[4][2][4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int g = 0; g < 2; ++g)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) acc[u][g][c] = 0.0;
+    for (int t0 = 0; t0 < dm; t0 += K1_BTT) {
+        const int tt = min(K1_BTT, dm - t0);         // a multiple of 4
+        __syncthreads();
+        {   // psi_k rows g0 .. g0 + nb, columns t0 .. t0 + tt -> psT[t][g] (zero past nb), and
+            // phi_k of the block's users -> phT[t][u]: every load of the stage is issued
+            // before the first conversion (the staging is HBM-latency bound otherwise)
+            const int q4 = tt / 4;
+            constexpr int NPS = K1_BTT / 4 * GCH / K1_THREADS;      // psi float4 per thread (full stage)
+            constexpr int NPH = K1_BTT / 4 * K1_UB / K1_THREADS;    // phi float4 per thread
+            float4 v[NPS], f[NPH > 0 ? NPH : 1];
+#pragma unroll
+            for (int i = 0; i < NPS; ++i) {
+                const int x = threadIdx.x + i * K1_THREADS, c = x / GCH, g = x - c * GCH;
+                v[i] = (c < q4 && g < nb)
+                           ? __ldg(reinterpret_cast<const float4*>(psi + ((int64_t)k * b + g0 + g) * dm + t0) + c)
+                           : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+#pragma unroll
+            for (int i = 0; i < NPH; ++i) {
+                const int x = threadIdx.x + i * K1_THREADS, u = x / (K1_BTT / 4), c = x - u * (K1_BTT / 4);
+                f[i] = (c < q4 && u < nu)
+                           ? __ldg(reinterpret_cast<const float4*>(phi + (int64_t)(u0 + u) * d + (int64_t)k * dm + t0) + c)
+                           : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+#pragma unroll
+            for (int i = 0; i < NPS; ++i) {
+                const int x = threadIdx.x + i * K1_THREADS, c = x / GCH, g = x - c * GCH;
+                if (c < q4) {
+                    psT[(4 * c + 0) * GCH + g] = (double)v[i].x;
+                    psT[(4 * c + 1) * GCH + g] = (double)v[i].y;
+                    psT[(4 * c + 2) * GCH + g] = (double)v[i].z;
+                    psT[(4 * c + 3) * GCH + g] = (double)v[i].w;
+                }
+            }
+#pragma unroll
+            for (int i = 0; i < NPH; ++i) {
+                const int x = threadIdx.x + i * K1_THREADS, u = x / (K1_BTT / 4), c = x - u * (K1_BTT / 4);
+                if (c < q4) {
+                    phT[(4 * c + 0) * K1_UB + u] = (double)f[i].x;
+                    phT[(4 * c + 1) * K1_UB + u] = (double)f[i].y;
+                    phT[(4 * c + 2) * K1_UB + u] = (double)f[i].z;
+                    phT[(4 * c + 3) * K1_UB + u] = (double)f[i].w;
+                }
+            }
+        }
+        __syncthreads();
+#pragma unroll 2
+        for (int t = 0; t < tt; t += 4) {
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {               // t0 is a multiple of 4: chain = c
+                const double2 p = *reinterpret_cast<const double2*>(psT + (t + c) * GCH + 2 * gp);
+                const double2 f01 = *reinterpret_cast<const double2*>(phT + (t + c) * K1_UB + 4 * uq);
+                const double2 f23 = *reinterpret_cast<const double2*>(phT + (t + c) * K1_UB + 4 * uq + 2);
+                const double f[4] = {f01.x, f01.y, f23.x, f23.y};
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    acc[u][0][c] = fma(p.x, f[u], acc[u][0][c]);
+                    acc[u][1][c] = fma(p.y, f[u], acc[u][1][c]);
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int g = 0; g < 2; ++g) {
+            const int uu = 4 * uq + u, gg = 2 * gp + g;
+            if (uu < nu && gg < nb)
+                S[((int64_t)(u0 + uu) * m + k) * b + g0 + gg] =
+                    (float)((acc[u][g][0] + acc[u][g][1]) + (acc[u][g][2] + acc[u][g][3]));   // one rounding
+        }
+}
+
+template <int UB>
+static void launch_k1_blocked(const float* phi, const float* psi, int B, int d, int m, int b, float* S,
+                              cudaStream_t st) {
+    constexpr int GCH = K1_MAXOUT / UB;
+    const size_t smem = ((size_t)K1_BTT * GCH + (size_t)K1_BTT * UB) * sizeof(double);
+    ensure_max_smem(reinterpret_cast<const void*>(k1_blocked<UB>), (int)smem);
+    dim3 grid(m, (unsigned)ceil_div(B, UB), (unsigned)ceil_div(b, GCH));
+    launch_pdl(k1_blocked<UB>, grid, dim3(K1_THREADS), smem, st, phi, psi, B, d, m, b, S);
+    count_launch();
+    check_launch("k1_blocked");
+}
+
 template <int UB>
 static void launch_k1(const float* phi, const float* psi, int B, int d, int m, int b, float* S,
                       cudaStream_t st) {
@@ -154,6 +273,12 @@ void launch_subscores(const float* phi, const float* psi, int B, int d, int m, i
     static const int forced = [] { const char* e = getenv("PQTOPK_K1_UB"); return e ? atoi(e) : 0; }();
     // (measured, r02: C2 B = 128: 32 -> 14.8 us vs 16.8 at 4-16; C3 / C4: 16 best, 25 / 72 us)
     const int ub = forced ? forced : (B > 128 ? 16 : B >= 32 ? 32 : B >= 16 ? 16 : B >= 8 ? 8 : 4);
+    static const bool plain = getenv("PQTOPK_K1_PLAIN") != nullptr;   // diagnostics (A/B)
+    if (!plain && (d / m) % 4 == 0 && (ub == 32 || ub == 16)) {
+        if (ub == 32) launch_k1_blocked<32>(phi, psi, B, d, m, b, S, st);
+        else launch_k1_blocked<16>(phi, psi, B, d, m, b, S, st);
+        return;
+    }
     switch (ub) {
         case 32: launch_k1<32>(phi, psi, B, d, m, b, S, st); break;
         case 16: launch_k1<16>(phi, psi, B, d, m, b, S, st); break;

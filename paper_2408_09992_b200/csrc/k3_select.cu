@@ -69,12 +69,10 @@ k3_select(Src src, int64_t L, int K, int Kp, uint64_t* __restrict__ out_keys,
         // empty key 0 ranks last) and writes it straight to its sorted position
         __syncthreads();
         const uint64_t mine = tid < n ? keys[tid] : 0ull;
-        int rk = 0;
         // keys are unique for valid inputs; the index tie-break only keeps the
         // output slots distinct (memory-safe, every slot written) if a caller
         // passes a repeated (id, score) pair, which the contract forbids
-#pragma unroll 4
-        for (int j = 0; j < n; ++j) rk += (keys[j] > mine || (keys[j] == mine && j < tid)) ? 1 : 0;
+        const int rk = tid < n ? rank_in_smem(keys, n, tid) : n;
         const int nz = __syncthreads_count(mine != 0ull);
         if (mine != 0ull && rk < K) {
             if (out_ids) {

@@ -430,13 +430,21 @@ __global__ void __launch_bounds__(K6_THREADS) k6_query(const K6Args a) {
             const uint32_t g = __byte_perm(w, 0u, 0x4440u | (uint32_t)s);
             return *reinterpret_cast<const float*>(Tb + (size_t)k * bq * G * 4 + (size_t)g * (G * 4));
         };
-        float accs[J];
+        // two items' running sums per packed fp32x2 add (FADD2, RN: each lane of the
+        // pair is the same IEEE add as a scalar FADD, so the sums are unchanged)
+        static_assert(J % 2 == 0, "items in pairs");
+        float2 acc2[J / 2];
 #pragma unroll
-        for (int j = 0; j < J; ++j) accs[j] = look(0, cw[j][0], 0);
+        for (int j = 0; j < J / 2; ++j) acc2[j] = make_float2(look(0, cw[2 * j][0], 0), look(0, cw[2 * j + 1][0], 0));
 #pragma unroll
         for (int k = 1; k < M; ++k)
 #pragma unroll
-            for (int j = 0; j < J; ++j) accs[j] = accs[j] + look(k, cw[j][k >> 2], k & 3);
+            for (int j = 0; j < J / 2; ++j)
+                acc2[j] = __fadd2_rn(acc2[j], make_float2(look(k, cw[2 * j][k >> 2], k & 3),
+                                                          look(k, cw[2 * j + 1][k >> 2], k & 3)));
+        float accs[J];
+#pragma unroll
+        for (int j = 0; j < J / 2; ++j) { accs[2 * j] = acc2[j].x; accs[2 * j + 1] = acc2[j].y; }
         auto item_key = [&](float acc, int j) {        // R1-R3: +0 canonical score, global id
             const int64_t item = r0 + j * K6_THREADS + lrow;
             const uint32_t lid = a.perm ? (uint32_t)a.perm[item] : (uint32_t)item;

@@ -356,13 +356,20 @@ __global__ void __launch_bounds__(K7_THREADS, 1) k7_resident(const K7Args a) {
                     cw[q][0] = t.x; cw[q][1] = t.y; cw[q][2] = t.z; cw[q][3] = t.w;
                 }
             }
-            float acc[JB];
+            // two items per packed fp32x2 add (FADD2, RN: the same IEEE adds as scalar FADDs)
+            float2 acc2[JB / 2];
 #pragma unroll
-            for (int q = 0; q < JB; ++q) acc[q] = look(0, cw[q][0], 0);
+            for (int q = 0; q < JB / 2; ++q)
+                acc2[q] = make_float2(look(0, cw[2 * q][0], 0), look(0, cw[2 * q + 1][0], 0));
 #pragma unroll
             for (int k = 1; k < M; ++k)
 #pragma unroll
-                for (int q = 0; q < JB; ++q) acc[q] = acc[q] + look(k, cw[q][k >> 2], k & 3);
+                for (int q = 0; q < JB / 2; ++q)
+                    acc2[q] = __fadd2_rn(acc2[q], make_float2(look(k, cw[2 * q][k >> 2], k & 3),
+                                                              look(k, cw[2 * q + 1][k >> 2], k & 3)));
+            float acc[JB];
+#pragma unroll
+            for (int q = 0; q < JB / 2; ++q) { acc[2 * q] = acc2[q].x; acc[2 * q + 1] = acc2[q].y; }
 #pragma unroll
             for (int q = 0; q < JB; ++q) {
                 const int li = (jb + q) * K7_THREADS + lrow;

@@ -162,6 +162,29 @@ __device__ __forceinline__ uint64_t block_kth(const uint64_t* buf, int n, uint32
     return prefix;
 }
 
+// Rank of key buf[self] among buf[0..n) (shared memory, 16-byte aligned): keys
+// above it, plus equal keys at a lower index (only repeated keys, which the
+// callers' contracts forbid, tie -- the index keeps every output slot
+// distinct).  Sixteen keys per step through eight independent 128-bit loads:
+// the loop is load-latency bound otherwise.
+__device__ __forceinline__ int rank_in_smem(const uint64_t* buf, int n, int self) {
+    const uint64_t mine = buf[self];
+    int r0 = 0, r1 = 0;
+    int j = 0;
+    for (; j + 16 <= n; j += 16) {
+        ulonglong2 v[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) v[q] = *reinterpret_cast<const ulonglong2*>(buf + j + 2 * q);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            r0 += (v[q].x > mine || (v[q].x == mine && j + 2 * q < self)) ? 1 : 0;
+            r1 += (v[q].y > mine || (v[q].y == mine && j + 2 * q + 1 < self)) ? 1 : 0;
+        }
+    }
+    for (; j < n; ++j) r0 += (buf[j] > mine || (buf[j] == mine && j < self)) ? 1 : 0;
+    return r0 + r1;
+}
+
 // Block-level bitonic sort (descending) of s[0..n), n a power of two.
 __device__ __forceinline__ void block_bitonic_desc(uint64_t* s, int n) {
     for (int size = 2; size <= n; size <<= 1) {
