@@ -14,6 +14,8 @@ checked library).  Cases (SURVEY.md §5 "race detection"):
   latency   K2 v4 (B <= 4 through pq_score_topk) + K1 + K3
   k6grid    K6 fused query, cooperative grid mode
   k6clus    K6 fused query, cluster mode (cluster = 2)
+  k6pair    K6 on the colour-paired row-order codes (a long stream: 10M items)
+  k7        K7 fused query, chunk-resident codes (B = 1 and B = 2)
   merge     K3 pq_merge_topk over 8 shards
   subset    K5 subset V + exclusion lists
   recjpq    Alg. 2 on the GPU
@@ -84,6 +86,23 @@ def main(cases):
             i, s = pq.pq_search(idx, cu(F), cu(P), 10, S_out=S)
             torch.cuda.synchronize()
             same(i.cpu().numpy(), s.cpu().numpy(), *oracle.pq_topk(G, S.cpu().numpy(), 10), c)
+        elif c == "k6pair":
+            G, P, F = pqsynth.random_instance(9010, 10_000_019, 8, 256, 64, 1)
+            idx = pq.pq_create(G, b=256)
+            assert idx.search_plan(1, 64, 10)["variant"] == 5
+            S = torch.empty((1, 8, 256), dtype=torch.float32, device=dev)
+            i, s = pq.pq_search(idx, cu(F), cu(P), 10, S_out=S)
+            torch.cuda.synchronize()
+            same(i.cpu().numpy(), s.cpu().numpy(), *oracle.pq_topk(G, S.cpu().numpy(), 10), c)
+        elif c == "k7":
+            for B in (1, 2):
+                G, P, F = pqsynth.random_instance(9011 + B, 600_011, 8, 256, 64, B)
+                idx = pq.pq_create(G, b=256)
+                assert idx.search_plan(B, 64, 10)["variant"] == 7, idx.search_plan(B, 64, 10)
+                S = torch.empty((B, 8, 256), dtype=torch.float32, device=dev)
+                i, s = pq.pq_search(idx, cu(F), cu(P), 10, S_out=S)
+                torch.cuda.synchronize()
+                same(i.cpu().numpy(), s.cpu().numpy(), *oracle.pq_topk(G, S.cpu().numpy(), 10), c)
         elif c == "merge":
             G, P, F = pqsynth.random_instance(9006, 16_001, 4, 16, 16, 3)
             S = pq.pq_subscores(cu(F), cu(P))
@@ -130,8 +149,8 @@ if __name__ == "__main__":
     reps = 1
     if argv[:1] == ["--reps"]:
         reps, argv = int(argv[1]), argv[2:]
-    cases = argv or ["tiled16", "tiled8", "tiled4", "latency", "k6grid", "k6clus", "merge", "subset",
-                     "recjpq", "dense"]
+    cases = argv or ["tiled16", "tiled8", "tiled4", "latency", "k6grid", "k6clus", "k6pair", "k7", "merge",
+                     "subset", "recjpq", "dense"]
     import paper_2408_09992_b200 as _pq
     print("library:", _pq.lib_path(), flush=True)
     for _ in range(reps):
