@@ -248,8 +248,9 @@ size_t pq_search_workspace_bytes(pq_index idx, int32_t B, int32_t d, int32_t K);
  * then pq_score_topk(S, K).  seq_emb / subitem_emb may be HOST or device
  * pointers and ids / scores may be host or device: host buffers are copied
  * through the workspace on `stream` (pinned host memory makes the copies
- * asynchronous); with host outputs the call synchronises `stream` before
- * returning.
+ * asynchronous) -- except on the K7 path, where PINNED host ids / scores are
+ * written by the kernel in place (zero copy); with host outputs the call
+ * synchronises `stream` before returning.
  *
  * Small batches (1 <= B <= 4, m in {4, 8, 16}, K <= 512; the paper's serving
  * case) run as ONE kernel (K6): each thread-block cluster computes one

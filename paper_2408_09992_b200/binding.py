@@ -161,6 +161,8 @@ def _ws(nbytes: int, ws, device):
     if nbytes == 0:
         return None, 0
     if ws is None or ws.numel() < nbytes:
+        if device is None:
+            device = ws.device if ws is not None else torch.device("cuda", torch.cuda.current_device())
         ws = torch.empty(nbytes, dtype=torch.uint8, device=device)
     return ws, ws.numel()
 
@@ -171,6 +173,7 @@ class PQIndex:
     def __init__(self, handle: int, N: int, m: int, b: int, id_base: int):
         self._h = ctypes.c_void_p(handle)
         self.N, self.m, self.b, self.id_base = N, m, b, id_base
+        self._search_ws = {}                     # (B, d, K) -> pq_search workspace bytes (per tuning)
 
     @property
     def handle(self):
@@ -232,6 +235,7 @@ class PQIndex:
                    cluster=0):
         t = Tuning(variant, ctas, warps, chunks, users_per_row, shrink_watermark, cluster)
         _check(load_library().pq_set_tuning(self._h, ctypes.byref(t)))
+        self._search_ws.clear()                  # the plans (and their workspaces) depend on it
 
     def timing_enable(self, on: bool = True):
         _check(load_library().pq_timing_enable(self._h, 1 if on else 0))
@@ -378,7 +382,9 @@ def pq_search(index: PQIndex, seq_emb, subitem_emb, K: int, ws=None, ids=None, s
     (optional CUDA fp32 [B][m][b]) receives the sub-id scores."""
     torch = _torch()
     B, d = int(seq_emb.shape[0]), int(seq_emb.shape[1])
-    dev = torch.device("cuda", torch.cuda.current_device())
+    dev = None
+    if ids is None or scores is None or ws is None:
+        dev = torch.device("cuda", torch.cuda.current_device())
     if ids is None:
         ids = torch.empty((B, K), dtype=torch.int32, device=dev)
     if scores is None:
@@ -386,7 +392,10 @@ def pq_search(index: PQIndex, seq_emb, subitem_emb, K: int, ws=None, ids=None, s
     if S_out is not None:
         _need_cuda(S_out, "S_out")
     L = load_library()
-    nb = int(L.pq_search_workspace_bytes(index.handle, B, d, K)) if B > 0 and 0 < K <= MAX_K else 0
+    nb = index._search_ws.get((B, d, K))       # (a serving loop asks for the same shape every call)
+    if nb is None:
+        nb = int(L.pq_search_workspace_bytes(index.handle, B, d, K)) if B > 0 and 0 < K <= MAX_K else 0
+        index._search_ws[(B, d, K)] = nb
     ws, wsb = _ws(nb, ws, dev)
     _check(L.pq_search_ex(index.handle, ctypes.c_void_p(_ptr(seq_emb)), ctypes.c_void_p(_ptr(subitem_emb)),
                           B, d, K, 0 if fused else SEARCH_NO_FUSED,

@@ -57,6 +57,9 @@ struct K7Args {
     uint32_t id_base;
     int chunks;                    // per user
     int chunk_items;               // multiple of 16, <= K7_THREADS * K7_JMAX
+    int solo;                      // 1: one CTA per user (chunks == 1, d/m = 4 or 8): the CTA
+                                   // computes its user's whole S into its table and writes the answer
+                                   // itself -- no exchange, no reset kernel, no ticket
 };
 
 constexpr int K7_THREADS = 512;
@@ -231,6 +234,57 @@ __global__ void __launch_bounds__(K7_THREADS, 1) k7_resident(const K7Args a) {
     }
     bool issued = false;
 
+    if (a.solo) {
+        // ---- solo: this user's whole S, four entries per thread at a time with all
+        // their Psi / phi loads in flight; one thread per entry, K1's four fp64
+        // chains (R5b), written straight into the G table copies
+        pdl_wait();                                    // phi may come from the stream predecessor
+        const int rot = lane * G / 32;
+        const int q4 = a.L / 4;                        // <= 2
+        const float* phu = a.phi + (int64_t)u * a.d;
+        for (int eb = 0; eb < E; eb += 4 * K7_THREADS) {
+            float4 pv[4][2], fv[4][2];
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                const int e = eb + r * K7_THREADS + tid;
+                const bool ok = e < E;
+                const float4* pr = reinterpret_cast<const float4*>(a.psi + (int64_t)(ok ? e : 0) * a.L);
+                const float4* fr = reinterpret_cast<const float4*>(phu + (int64_t)((ok ? e : 0) / bq) * a.L);
+#pragma unroll
+                for (int i = 0; i < 2; ++i)
+                    if (i < q4) { pv[r][i] = __ldg(pr + i); fv[r][i] = __ldg(fr + i); }
+            }
+            if (tid == 0 && !issued) { issue_codes(); issued = true; }
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                const int e = eb + r * K7_THREADS + tid;
+                double x0 = 0.0, x1 = 0.0, x2 = 0.0, x3 = 0.0;
+#pragma unroll
+                for (int i = 0; i < 2; ++i)
+                    if (i < q4) {
+                        x0 = fma((double)pv[r][i].x, (double)fv[r][i].x, x0);
+                        x1 = fma((double)pv[r][i].y, (double)fv[r][i].y, x1);
+                        x2 = fma((double)pv[r][i].z, (double)fv[r][i].z, x2);
+                        x3 = fma((double)pv[r][i].w, (double)fv[r][i].w, x3);
+                    }
+                if (e < E) {
+                    const float v = (float)((x0 + x1) + (x2 + x3));
+                    if (a.S_out) a.S_out[(int64_t)u * E + e] = v;
+                    if constexpr (G >= 4) {
+                        constexpr int NQ = G / 4;
+                        const float4 v4 = make_float4(v, v, v, v);
+                        float4* dst = reinterpret_cast<float4*>(T + (size_t)e * G);
+#pragma unroll
+                        for (int c = 0; c < NQ; ++c) dst[(c + rot) % NQ] = v4;
+                    } else {
+#pragma unroll
+                        for (int c = 0; c < G; ++c) T[(size_t)e * G + c] = v;
+                    }
+                }
+            }
+        }
+        if (tid == 0 && !issued) issue_codes();
+    } else
     // ---- (1) this CTA's share of the B*E sub-id scores, K1's fp64 order (R5b)
     {
         const int EB = a.B * E;
@@ -272,6 +326,7 @@ __global__ void __launch_bounds__(K7_THREADS, 1) k7_resident(const K7Args a) {
             }
         }
     }
+    if (!a.solo) {
     if (tid == 0 && !issued) issue_codes();
     asm volatile("griddepcontrol.wait;" ::: "memory");
     stamp(2);
@@ -317,6 +372,7 @@ __global__ void __launch_bounds__(K7_THREADS, 1) k7_resident(const K7Args a) {
                 }
             }
         }
+    }
     }
     stamp(3);
     __syncthreads();                                   // table ready
@@ -446,6 +502,18 @@ __global__ void __launch_bounds__(K7_THREADS, 1) k7_resident(const K7Args a) {
     }
     __syncthreads();
     stamp(6);
+    if (a.solo) {                                      // the user's answer: sorted top K -> ids / scores
+        const int n = count;
+        uint64_t* res = fk + K7_THREADS;
+        k7_topk(cbuf, n, K, fk, &count, hist, sc, res);
+        __syncthreads();
+        for (int j = tid; j < K; j += K7_THREADS) {
+            const uint64_t key = j < n ? res[j] : 0ull;
+            a.ids[(int64_t)u * K + j] = key ? key_id(key) : -1;
+            a.scores[(int64_t)u * K + j] = key ? key_score(key) : -INFINITY;
+        }
+        return;
+    }
     {
         const int n = count;
         uint64_t* out = a.cand + ((int64_t)u * a.chunks + chunk) * K;
@@ -594,8 +662,14 @@ bool k7_resident_plan(const pq_index_s* idx, int B, int d, int K, K6Plan& p) {
     const int cap = idx->num_sms / B;                  // one CTA per SM, one wave
     if (cap < 1) return false;
     int64_t ch = std::max<int64_t>(1, std::min<int64_t>(cap, ceil_div(N, 512)));   // >= 512 items per CTA
-    if (t.chunks > 0) ch = std::min<int64_t>(t.chunks, cap);
     const size_t budget = idx->smem_optin - k7_static_bytes();
+    {   // solo (one CTA per user scores the whole catalogue) when it fits: tiny catalogues (C1)
+        const int L = d / m;
+        const int64_t c1 = (int64_t)align_up((size_t)N, 16);
+        const size_t s1 = std::max(k7_tbytes(m, b, G, c1) + k7_rbytes(m, c1), align_up((size_t)K * 8, 128));
+        if (L % 4 == 0 && L <= 8 && c1 <= (int64_t)K7_THREADS * K7_JMAX && s1 <= budget) ch = 1;
+    }
+    if (t.chunks > 0) ch = std::min<int64_t>(t.chunks, cap);
     int64_t ci = 0;
     size_t smem = 0;
     for (;; --ch) {                                    // fewer chunks while the merge scratch does not fit
@@ -607,14 +681,18 @@ bool k7_resident_plan(const pq_index_s* idx, int B, int d, int K, K6Plan& p) {
     }
     ch = ceil_div(N, ci);
     if (ci > (int64_t)K7_THREADS * K7_JMAX || smem > budget) return false;
-    // auto: tiny catalogues (C1) are faster on K6, whose 256-thread CTAs ramp sooner
-    if (t.variant != 7 && ci < 2048) return false;
+    // solo (one CTA per user, no exchange): every item of the user in one chunk
+    const int L = d / m;
+    const bool solo = ch == 1 && L % 4 == 0 && L <= 8;
+    // auto: small catalogues that still need several CTAs (K6's 256-thread CTAs ramp sooner)
+    if (t.variant != 7 && !solo && ci < 2048) return false;
     ensure_max_smem(reinterpret_cast<const void*>(fn), (int)smem);
     int per_sm = 0;
     PQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, K7_THREADS, smem));
     if (per_sm < 1 || (int64_t)per_sm * idx->num_sms < (int64_t)B * ch) return false;
     p = K6Plan{};
     p.resident = 1;
+    p.solo = solo ? 1 : 0;
     p.G = G;
     p.gridsync = 1;
     p.chunks = (int)ch;
@@ -646,21 +724,36 @@ void launch_k7_resident(const pq_index_s* idx, const K6Plan& p, const float* phi
     a.id_base = (uint32_t)idx->id_base;
     a.chunks = p.chunks;
     a.chunk_items = (int)p.chunk_items;
-    k7_reset<<<1, 256, 0, st>>>(reinterpret_cast<uint4*>(w), (int)(rb / 16));
-    count_launch();
-    check_launch("k7_reset");
+    a.solo = p.solo;
+    if (!p.solo) {
+        k7_reset<<<1, 256, 0, st>>>(reinterpret_cast<uint4*>(w), (int)(rb / 16));
+        count_launch();
+        check_launch("k7_reset");
+    }
     cudaLaunchConfig_t cfg{};
     cudaLaunchAttribute at[2];
     cfg.gridDim = dim3((unsigned)p.grid);
     cfg.blockDim = dim3(K7_THREADS);
     cfg.dynamicSmemBytes = p.smem;
     cfg.stream = st;
-    at[0].id = cudaLaunchAttributeCooperative;
-    at[0].val.cooperative = 1;
-    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[1].val.programmaticStreamSerializationAllowed = 1;
+    // solo CTAs never wait on each other: no cooperative launch (diagnostics:
+    // PQTOPK_K7_COOP=0/1 forces it off/on for A/B)
+    static const int coop_env = getenv("PQTOPK_K7_COOP") ? atoi(getenv("PQTOPK_K7_COOP")) : -1;
+    const bool coop = coop_env >= 0 ? coop_env != 0 : !p.solo;
+    int na = 0;
+    if (coop) {
+        at[na].id = cudaLaunchAttributeCooperative;
+        at[na].val.cooperative = 1;
+        ++na;
+    }
+    static const bool no_pdl = getenv("PQTOPK_K7_NO_PDL") != nullptr;   // diagnostics (A/B)
+    if (!no_pdl) {
+        at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[na].val.programmaticStreamSerializationAllowed = 1;
+        ++na;
+    }
     cfg.attrs = at;
-    cfg.numAttrs = 2;
+    cfg.numAttrs = na;
     const char* tf = getenv("PQTOPK_K6_TRACE");
     if (tf && *tf) {
         PQ_CUDA(cudaMalloc(&a.trace, (size_t)p.grid * 32 * 8));

@@ -51,6 +51,7 @@ static bool is_device_ptr(const void* p) {
     return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
 }
 
+
 static void need(bool c, const char* msg) {
     if (!c) fail(PQ_ERR_INVALID_ARG, msg);
 }
@@ -539,19 +540,47 @@ pq_status pq_search_ex(pq_index idx, const float* seq_emb, const float* subitem_
     char* rest = c.base + c.off;
     const float* phi = seq_emb;
     const float* psi = subitem_emb;
-    if (!is_device_ptr(seq_emb)) {
+    K6Plan kp;
+    const bool fused = use_k6(idx, B, d, K, flags, kp);
+    // K7 writes pinned host ids / scores in place (zero copy: 8 B per result over
+    // the host link instead of a DMA per buffer and its API call); pinned host
+    // phi is read in place only when PQTOPK_ZC_PHI=1 (diagnostics: the kernel's
+    // many small host reads measured slower than one DMA)
+    static const bool zc_phi = [] { const char* e = getenv("PQTOPK_ZC_PHI"); return e && atoi(e) == 1; }();
+    static const bool zc_off = getenv("PQTOPK_ZC_OFF") != nullptr;
+    const bool zc = fused && kp.resident && !zc_off;
+    cudaPointerAttributes pa;
+    auto kind = [&](const void* p) -> int {            // 0 device, 1 pinned host (pa.devicePointer), 2 pageable
+        if (cudaPointerGetAttributes(&pa, p) != cudaSuccess) { cudaGetLastError(); return 2; }
+        if (pa.type == cudaMemoryTypeDevice || pa.type == cudaMemoryTypeManaged) return 0;
+        return pa.type == cudaMemoryTypeHost && pa.devicePointer ? 1 : 2;
+    };
+    const int k_phi = kind(seq_emb);
+    if (k_phi == 1 && zc && zc_phi) {
+        phi = static_cast<const float*>(pa.devicePointer);
+    } else if (k_phi != 0) {
         PQ_CUDA(cudaMemcpyAsync(phi_st, seq_emb, (size_t)B * d * 4, cudaMemcpyHostToDevice, st));
         phi = phi_st;
     }
-    if (!is_device_ptr(subitem_emb)) {
+    if (kind(subitem_emb) != 0) {
         PQ_CUDA(cudaMemcpyAsync(psi_st, subitem_emb, (size_t)b * d * 4, cudaMemcpyHostToDevice, st));
         psi = psi_st;
     }
-    const bool host_ids = !is_device_ptr(ids), host_sc = !is_device_ptr(scores);
+    const int k_ids = kind(ids);
+    void* m_ids = k_ids == 1 ? pa.devicePointer : nullptr;
+    const int k_sc = kind(scores);
+    void* m_sc = k_sc == 1 ? pa.devicePointer : nullptr;
+    bool host_ids = k_ids != 0, host_sc = k_sc != 0;
     int32_t* ids_d = host_ids ? ids_st : ids;
     float* sc_d = host_sc ? sc_st : scores;
-    K6Plan kp;
-    if (use_k6(idx, B, d, K, flags, kp)) {
+    bool sync_out = false;                             // host outputs written in place: sync only
+    if (zc && m_ids && m_sc) {
+        ids_d = static_cast<int32_t*>(m_ids);
+        sc_d = static_cast<float*>(m_sc);
+        host_ids = host_sc = false;
+        sync_out = true;
+    }
+    if (fused) {
         pq_index_s::EvTriple ev{};
         if (idx->timing) {
             PQ_CUDA(cudaEventCreate(&ev.a)); PQ_CUDA(cudaEventCreate(&ev.b)); PQ_CUDA(cudaEventCreate(&ev.c));
@@ -571,7 +600,7 @@ pq_status pq_search_ex(pq_index idx, const float* seq_emb, const float* subitem_
     }
     if (host_ids) PQ_CUDA(cudaMemcpyAsync(ids, ids_st, (size_t)B * K * 4, cudaMemcpyDeviceToHost, st));
     if (host_sc) PQ_CUDA(cudaMemcpyAsync(scores, sc_st, (size_t)B * K * 4, cudaMemcpyDeviceToHost, st));
-    if (host_ids || host_sc) PQ_CUDA(cudaStreamSynchronize(st));
+    if (host_ids || host_sc || sync_out) PQ_CUDA(cudaStreamSynchronize(st));
     PQ_API_END
 }
 

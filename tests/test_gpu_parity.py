@@ -496,6 +496,31 @@ def test_fused_query_graph_replay_and_host_buffers(pq, torch, orc):
     assert_same(oi.numpy(), os_.numpy(), *ref, "host buffers")
 
 
+@pytest.mark.gpu
+def test_search_host_buffers_zero_copy(pq, torch, orc):
+    """pq_search through K7 with pinned host ids / scores (written in place by the
+    kernel), with pageable host buffers (staged copies) and mixed host / device
+    buffers: the same bits as the oracle every time."""
+    G, P, F = pqsynth.random_instance(541, 700_001, 8, 256, 64, 2)
+    idx = pq.pq_create(G, b=256)
+    assert idx.search_plan(2, 64, 10)["variant"] == 7
+    Pd = cuda(torch, P)
+    S = pq.pq_subscores(cuda(torch, F), Pd)
+    ref = orc.pq_topk(G, S.cpu().numpy(), 10)
+    Fp = torch.from_numpy(F).pin_memory()
+    for pin_out in (True, False):
+        oi = torch.full((2, 10), -7, dtype=torch.int32)
+        os_ = torch.full((2, 10), float("nan"), dtype=torch.float32)
+        if pin_out:
+            oi, os_ = oi.pin_memory(), os_.pin_memory()
+        for phi in (Fp, torch.from_numpy(F.copy())):
+            oi.fill_(-7)
+            pq.pq_search(idx, phi, Pd, 10, ids=oi, scores=os_)
+            assert_same(oi.numpy(), os_.numpy(), *ref, f"pin_out={pin_out} pinned_phi={phi.is_pinned()}")
+    di, ds = pq.pq_search(idx, Fp, Pd, 10)                  # pinned phi, device outputs
+    assert_same(di.cpu().numpy(), ds.cpu().numpy(), *ref, "device outputs")
+
+
 SUBSET_CASES = [
     # seed, N, m, b, B, K, nV, dist
     (600, 100_000, 8, 256, 3, 10, 5_000, "uniform"),      # small batch (v4 + row map)
