@@ -133,9 +133,11 @@ __global__ void __launch_bounds__(K6_THREADS) k6_query(const K6Args a) {
     cg::cluster_group cluster = cg::this_cluster();
     const int crank = (int)cluster.block_rank(), CL = (int)cluster.num_blocks();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    // colour-paired rows: lanes l and l + 16 take the complementary rows 2p, 2p + 1
-    // (opposite parity at every split -> opposite bank halves of the table copies)
-    const int lrow = (int)(threadIdx.x & ~31u) + (a.cmap ? (((lane & 15) << 1) | (lane >> 4)) : lane);
+    // lanes 2i and 2i + 1 share table copy i (G = 16; copy = lane * G / 32 in
+    // general): on colour-paired rows they hold the complementary rows 2p, 2p + 1
+    // (opposite parity at every split -> opposite bank halves of the copy), and the
+    // code words of a warp stay one contiguous 256-byte block
+    const int lrow = (int)threadIdx.x;
     auto src = [&](int e) { return a.cmap ? e - e % (BB > 0 ? BB : a.b) + (int)__ldg(a.cmap + e) : e; };
     const int u = blockIdx.x / a.chunks;
     const int chunk = blockIdx.x % a.chunks;
@@ -400,7 +402,7 @@ __global__ void __launch_bounds__(K6_THREADS) k6_query(const K6Args a) {
 
     // ---- (2)+(3) gather-sum over the chunk (lane = item), CTA-wide exact selection
     float tf = -INFINITY;
-    const float* Tl = T + lane % G;
+    const float* Tl = T + ((lane * G) >> 5);
     int slot = 0;
     uint32_t phase = 0;
     for (int64_t r = 0; r < rounds; ++r) {
