@@ -736,22 +736,18 @@ void launch_k7_resident(const pq_index_s* idx, const K6Plan& p, const float* phi
     cfg.blockDim = dim3(K7_THREADS);
     cfg.dynamicSmemBytes = p.smem;
     cfg.stream = st;
-    // solo CTAs never wait on each other: no cooperative launch (diagnostics:
-    // PQTOPK_K7_COOP=0/1 forces it off/on for A/B)
-    static const int coop_env = getenv("PQTOPK_K7_COOP") ? atoi(getenv("PQTOPK_K7_COOP")) : -1;
-    const bool coop = coop_env >= 0 ? coop_env != 0 : !p.solo;
+    // CTAs that poll each other's sub-id scores must be co-resident: a cooperative
+    // launch; solo CTAs never wait on each other (measured: neither attribute
+    // changes the C1 / C2a step)
     int na = 0;
-    if (coop) {
+    if (!p.solo) {
         at[na].id = cudaLaunchAttributeCooperative;
         at[na].val.cooperative = 1;
         ++na;
     }
-    static const bool no_pdl = getenv("PQTOPK_K7_NO_PDL") != nullptr;   // diagnostics (A/B)
-    if (!no_pdl) {
-        at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-        at[na].val.programmaticStreamSerializationAllowed = 1;
-        ++na;
-    }
+    at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;   // after k7_reset / the producer of phi
+    at[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
     cfg.attrs = at;
     cfg.numAttrs = na;
     const char* tf = getenv("PQTOPK_K6_TRACE");
