@@ -977,7 +977,13 @@ void plan_k2_tiled(const pq_index_s* idx, int B, int K, K2Plan& p) {
     p.tm = (sh.m_v / sh.ps) > 1 ? sh.m_v - sh.ps : 0;
     p.n_groups = (int)ceil_div(B, R);
     const int TR = k2_tiled_rows_per_tile(R);
-    p.cap = (int)align_up((size_t)(2 * K + (2 * k2_slack() + 1) * TR + 96), 32);
+    // shrink watermark: 2K + 64, but >= 2048 for K <= 16 -- with a small K the early,
+    // weak-threshold tiles would otherwise shrink (a CTA barrier that absorbs the
+    // warps' skew) again and again: C2 K2 0.2117 -> 0.2067 ms; larger watermarks cost
+    // C3 (K = 100) time in the end-of-unit selection (r03 A/B, PQTOPK_K2_WMIN)
+    static const int wmin = getenv("PQTOPK_K2_WMIN") ? atoi(getenv("PQTOPK_K2_WMIN")) : 0;
+    const int wm_auto = std::max(std::max(2 * K + 64, K <= 16 ? 2048 : 0), wmin);
+    p.cap = (int)align_up((size_t)(wm_auto + (2 * k2_slack() + 1) * TR + 32), 32);
     p.smem = k2_tiled_smem(sh, p.W);
     K2TFn fn = tiled_fn_shape(sh, p.W);
     if (!fn) fail(PQ_ERR_UNSUPPORTED, "tiled scoring kernel: unsupported shape");
