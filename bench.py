@@ -5,9 +5,10 @@
     python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 bench.py --gpus N
 
 A step is one pass of the whole hot path over one batch: K1 sub-id scores
-(pq_subscores) -> K2 fused gather-sum-select -> K3 merge (pq_score_topk), and
-for N > 1 GPUs (item-sharded catalogue) an NCCL all-gather of the B x K local
-results followed by pq_merge_topk.  Metric (BASELINE.json): user-item
+(pq_subscores) -> K2 fused gather-sum-select -> K3 merge (pq_score_topk) for
+batches, ONE fused launch (pq_search: K7, or K6 for long streams) for B <= 4,
+and for N > 1 GPUs (item-sharded catalogue) an NCCL all-gather of the B x K
+local results followed by pq_merge_topk.  Metric (BASELINE.json): user-item
 scores/s = B * N_items / step time (whole job), plus top-K queries/s.
 
 Timing: W untimed warm-up steps; K timed steps bracketed by barrier +

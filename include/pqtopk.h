@@ -253,11 +253,15 @@ size_t pq_search_workspace_bytes(pq_index idx, int32_t B, int32_t d, int32_t K);
  * synchronises `stream` before returning.
  *
  * Small batches (1 <= B <= 4, m in {4, 8, 16}, K <= 512; the paper's serving
- * case) run as ONE kernel (K6): each thread-block cluster computes one
- * user's S (Eq. 4, the same fp64 order and single rounding as pq_subscores, so
- * S is bit-identical), scores its item chunks (Eq. 5) and selects; the last
- * CTA of each user merges the chunk lists (Alg. 1).  Results are
- * bit-identical to the multi-kernel path.
+ * case) run as ONE kernel: K7 when each CTA's item chunk fits in shared
+ * memory (one CTA per user for tiny catalogues), else K6 (a streamed code
+ * ring).  The grid computes S (Eq. 4, the same fp64 order and single rounding
+ * as pq_subscores, so S is bit-identical), scores its item chunks (Eq. 5) and
+ * selects; the last CTA of each user merges the chunk lists (Alg. 1).
+ * Results are bit-identical to the multi-kernel path.  K7 and K6 (grid mode)
+ * are cooperative launches preceded by a one-CTA reset kernel (the call's
+ * counters live in the workspace); they assume no other work occupies the
+ * GPU's SMs for their duration.
  */
 pq_status pq_search(pq_index idx, const float* seq_emb, const float* subitem_emb,
                     int32_t B, int32_t d, int32_t K, void* ws, size_t ws_bytes,
