@@ -160,7 +160,7 @@ pq_status pq_plan_info(pq_index idx, int32_t B, int32_t K, int64_t out[8]);
 /*
  * The plan pq_search would use for (B, d, K): out[0] = 5 when the fused K6
  * kernel runs, 7 when the fused chunk-resident K7 kernel runs (then out[1] table copies G, out[2] CTAs per cluster (0: one
- * cooperative grid sharing S through L2), out[3]
+ * cooperative grid sharing S through L2; K7: CTAs per user cluster in its cluster mode), out[3]
  * warps per CTA, out[4] CTAs, out[5] item chunks per user, out[6] 0, out[7]
  * dynamic shared memory bytes), else exactly pq_plan_info(B, K).
  */

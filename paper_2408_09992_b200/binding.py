@@ -220,11 +220,12 @@ class PQIndex:
         return dict(zip(keys, [int(x) for x in out]))
 
     def search_plan(self, B: int, d: int, K: int) -> dict:
-        """The plan pq_search uses for (B, d, K): variant 5 = the fused K6 kernel."""
+        """The plan pq_search uses for (B, d, K): variant 5 = the fused K6 kernel, 7 = the
+        fused K7 kernel ("cluster" = CTAs per user cluster in its cluster mode, 0 = grid)."""
         out = (ctypes.c_int64 * 8)()
         _check(load_library().pq_search_plan_info(self._h, B, d, K, out))
         v = [int(x) for x in out]
-        if v[0] == 5:
+        if v[0] in (5, 7):
             keys = ["variant", "table_copies", "cluster", "warps", "ctas", "chunks", "tmem_splits", "smem_bytes"]
         else:
             keys = ["variant", "users_per_row", "users_per_group", "warps", "ctas", "chunks",

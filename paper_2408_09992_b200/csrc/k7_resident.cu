@@ -57,9 +57,10 @@ struct K7Args {
     uint32_t id_base;
     int chunks;                    // per user
     int chunk_items;               // multiple of 16, <= K7_THREADS * K7_JMAX
-    int solo;                      // 1: one CTA per user (chunks == 1, d/m = 4 or 8): the CTA
-                                   // computes its user's whole S into its table and writes the answer
-                                   // itself -- no exchange, no reset kernel, no ticket
+    int cl;                        // > 0: CLUSTER mode -- one thread-block cluster of cl CTAs per user
+                                   // (chunks == cl, d/m = 4 or 8): the CTAs split the user's S, exchange
+                                   // it through distributed shared memory, score their chunks and merge
+                                   // in rank 0 -- no global exchange, reset kernel or ticket; 0 = grid mode
 };
 
 constexpr int K7_THREADS = 512;
@@ -161,6 +162,15 @@ __device__ __forceinline__ void k7_topk(const uint64_t* buf, int n, int K, uint6
     }
 }
 
+__device__ __forceinline__ void cluster_arrive() { asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory"); }
+__device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory"); }
+// this CTA's shared address `local` in cluster CTA `rank`
+__device__ __forceinline__ uint32_t dsmem_addr(uint32_t local, int rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local), "r"(rank));
+    return r;
+}
+
 __device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
     unsigned long long v;
     asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
@@ -234,22 +244,26 @@ __global__ void __launch_bounds__(K7_THREADS, 1) k7_resident(const K7Args a) {
     }
     bool issued = false;
 
-    if (a.solo) {
-        // ---- solo: this user's whole S, four entries per thread at a time with all
-        // their Psi / phi loads in flight; one thread per entry, K1's four fp64
-        // chains (R5b), written straight into the G table copies
+    // cluster mode: the staging of the user's E sub-id scores (then rank 0's merge area)
+    float* Sst = reinterpret_cast<float*>(Rg + align_up((size_t)a.chunk_items * MP, 128));
+    if (a.cl) {
+        // ---- cluster mode: rank r computes entries [r E / cl, (r + 1) E / cl) of its user,
+        // four per thread with all their Psi / phi loads in flight (one thread per
+        // entry, K1's four fp64 chains, R5b), and stores each into the staging of
+        // every CTA of the cluster (distributed shared memory)
         pdl_wait();                                    // phi may come from the stream predecessor
-        const int rot = lane * G / 32;
         const int q4 = a.L / 4;                        // <= 2
         const float* phu = a.phi + (int64_t)u * a.d;
-        for (int eb = 0; eb < E; eb += 4 * K7_THREADS) {
+        const int per = E / a.cl, e_lo = chunk * per, e_hi = e_lo + per;
+        const uint32_t sst = smem_u32(Sst);
+        for (int eb = e_lo; eb < e_hi; eb += 4 * K7_THREADS) {
             float4 pv[4][2], fv[4][2];
 #pragma unroll
             for (int r = 0; r < 4; ++r) {
                 const int e = eb + r * K7_THREADS + tid;
-                const bool ok = e < E;
-                const float4* pr = reinterpret_cast<const float4*>(a.psi + (int64_t)(ok ? e : 0) * a.L);
-                const float4* fr = reinterpret_cast<const float4*>(phu + (int64_t)((ok ? e : 0) / bq) * a.L);
+                const bool ok = e < e_hi;
+                const float4* pr = reinterpret_cast<const float4*>(a.psi + (int64_t)(ok ? e : e_lo) * a.L);
+                const float4* fr = reinterpret_cast<const float4*>(phu + (int64_t)((ok ? e : e_lo) / bq) * a.L);
 #pragma unroll
                 for (int i = 0; i < 2; ++i)
                     if (i < q4) { pv[r][i] = __ldg(pr + i); fv[r][i] = __ldg(fr + i); }
@@ -267,23 +281,34 @@ __global__ void __launch_bounds__(K7_THREADS, 1) k7_resident(const K7Args a) {
                         x2 = fma((double)pv[r][i].z, (double)fv[r][i].z, x2);
                         x3 = fma((double)pv[r][i].w, (double)fv[r][i].w, x3);
                     }
-                if (e < E) {
+                if (e < e_hi) {
                     const float v = (float)((x0 + x1) + (x2 + x3));
                     if (a.S_out) a.S_out[(int64_t)u * E + e] = v;
-                    if constexpr (G >= 4) {
-                        constexpr int NQ = G / 4;
-                        const float4 v4 = make_float4(v, v, v, v);
-                        float4* dst = reinterpret_cast<float4*>(T + (size_t)e * G);
-#pragma unroll
-                        for (int c = 0; c < NQ; ++c) dst[(c + rot) % NQ] = v4;
-                    } else {
-#pragma unroll
-                        for (int c = 0; c < G; ++c) T[(size_t)e * G + c] = v;
-                    }
+                    for (int q = 0; q < a.cl; ++q)
+                        asm volatile("st.shared::cluster.f32 [%0], %1;" :: "r"(dsmem_addr(sst + 4u * (uint32_t)e, q)),
+                                     "f"(v) : "memory");
                 }
             }
         }
         if (tid == 0 && !issued) issue_codes();
+        cluster_arrive();                              // this CTA's share is in every staging
+        cluster_wait();                                // ... and every share is in this CTA's
+        // G copies of each entry into the local table (bank-rotated stores)
+        const int rot = lane * G / 32;
+        for (int e = tid; e < E; e += K7_THREADS) {
+            const float v = Sst[e];
+            if constexpr (G >= 4) {
+                constexpr int NQ = G / 4;
+                const float4 v4 = make_float4(v, v, v, v);
+                float4* dst = reinterpret_cast<float4*>(T + (size_t)e * G);
+#pragma unroll
+                for (int c = 0; c < NQ; ++c) dst[(c + rot) % NQ] = v4;
+            } else {
+#pragma unroll
+                for (int c = 0; c < G; ++c) T[(size_t)e * G + c] = v;
+            }
+        }
+        cluster_arrive();                              // staging read: rank 0 may reuse its own (merge)
     } else
     // ---- (1) this CTA's share of the B*E sub-id scores, K1's fp64 order (R5b)
     {
@@ -326,7 +351,7 @@ __global__ void __launch_bounds__(K7_THREADS, 1) k7_resident(const K7Args a) {
             }
         }
     }
-    if (!a.solo) {
+    if (!a.cl) {
     if (tid == 0 && !issued) issue_codes();
     asm volatile("griddepcontrol.wait;" ::: "memory");
     stamp(2);
@@ -502,13 +527,32 @@ __global__ void __launch_bounds__(K7_THREADS, 1) k7_resident(const K7Args a) {
     }
     __syncthreads();
     stamp(6);
-    if (a.solo) {                                      // the user's answer: sorted top K -> ids / scores
+    if (a.cl) {
+        // cluster mode: this chunk's sorted top K -> rank 0's merge area (its staging,
+        // read by rank 0 only before the second cluster arrive); rank 0 merges the
+        // cl * K keys (0 = empty ranks last) and writes the user's ids / scores
         const int n = count;
         uint64_t* res = fk + K7_THREADS;
         k7_topk(cbuf, n, K, fk, &count, hist, sc, res);
         __syncthreads();
+        cluster_wait();                                // every CTA is past its staging reads
+        uint64_t* mrg = reinterpret_cast<uint64_t*>(Sst);
+        const uint32_t m0 = smem_u32(mrg);
         for (int j = tid; j < K; j += K7_THREADS) {
             const uint64_t key = j < n ? res[j] : 0ull;
+            asm volatile("st.shared::cluster.u64 [%0], %1;" :: "r"(dsmem_addr(m0 + 8u * (uint32_t)(chunk * K + j), 0)),
+                         "l"(key) : "memory");
+        }
+        cluster_arrive();
+        cluster_wait();                                // rank 0's merge area complete
+        if (chunk != 0) return;
+        uint64_t* out = fk + K7_THREADS;
+        for (int j = tid; j < K; j += K7_THREADS) out[j] = 0ull;   // slots past the real keys stay empty
+        __syncthreads();
+        k7_topk(mrg, a.cl * K, K, fk, &count, hist, sc, out);
+        __syncthreads();
+        for (int j = tid; j < K; j += K7_THREADS) {
+            const uint64_t key = out[j];
             a.ids[(int64_t)u * K + j] = key ? key_id(key) : -1;
             a.scores[(int64_t)u * K + j] = key ? key_score(key) : -INFINITY;
         }
@@ -663,12 +707,21 @@ bool k7_resident_plan(const pq_index_s* idx, int B, int d, int K, K6Plan& p) {
     if (cap < 1) return false;
     int64_t ch = std::max<int64_t>(1, std::min<int64_t>(cap, ceil_div(N, 512)));   // >= 512 items per CTA
     const size_t budget = idx->smem_optin - k7_static_bytes();
-    {   // solo (one CTA per user scores the whole catalogue) when it fits: tiny catalogues (C1)
+    // cluster mode (one cluster of cl CTAs per user, no global exchange) when a user's
+    // catalogue fits cl chunks: small catalogues (C1); cl = 8 unless the catalogue is tiny
+    int cl = 0;
+    {
         const int L = d / m;
-        const int64_t c1 = (int64_t)align_up((size_t)N, 16);
-        const size_t s1 = std::max(k7_tbytes(m, b, G, c1) + k7_rbytes(m, c1), align_up((size_t)K * 8, 128));
-        if (L % 4 == 0 && L <= 8 && c1 <= (int64_t)K7_THREADS * K7_JMAX && s1 <= budget) ch = 1;
+        const int want = (int)std::min<int64_t>(8, std::max<int64_t>(1, N / 1024));
+        for (int c = 8; c >= 1 && !cl; c >>= 1) {
+            if (c > want || (m * b) % c || (int64_t)B * c > idx->num_sms || c * K > 256) continue;
+            const int64_t cc = (int64_t)align_up((size_t)ceil_div(N, c), 16);
+            const size_t sc1 = k7_tbytes(m, b, G, cc) + k7_rbytes(m, cc) + align_up((size_t)m * b * 4, 128);
+            if (L % 4 == 0 && L <= 8 && cc <= (int64_t)K7_THREADS * K7_JMAX && sc1 <= budget) cl = c;
+        }
+        if (t.chunks > 0 || t.variant == 5) cl = 0;
     }
+    if (cl) ch = cl;
     if (t.chunks > 0) ch = std::min<int64_t>(t.chunks, cap);
     int64_t ci = 0;
     size_t smem = 0;
@@ -681,18 +734,20 @@ bool k7_resident_plan(const pq_index_s* idx, int B, int d, int K, K6Plan& p) {
     }
     ch = ceil_div(N, ci);
     if (ci > (int64_t)K7_THREADS * K7_JMAX || smem > budget) return false;
-    // solo (one CTA per user, no exchange): every item of the user in one chunk
-    const int L = d / m;
-    const bool solo = ch == 1 && L % 4 == 0 && L <= 8;
-    // auto: small catalogues that still need several CTAs (K6's 256-thread CTAs ramp sooner)
-    if (t.variant != 7 && !solo && ci < 2048) return false;
+    if (cl) {                                          // the staging / merge area after R
+        smem = k7_tbytes(m, b, G, ci) + k7_rbytes(m, ci) + align_up((size_t)m * b * 4, 128);
+        if (smem > budget || ceil_div(N, ci) > cl) return false;
+        ch = cl;                                       // whole clusters (a trailing CTA may hold no items)
+    }
+    // auto: grid-mode catalogues too small for >= 2048 items per CTA go to K6
+    if (t.variant != 7 && !cl && ci < 2048) return false;
     ensure_max_smem(reinterpret_cast<const void*>(fn), (int)smem);
     int per_sm = 0;
     PQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, K7_THREADS, smem));
     if (per_sm < 1 || (int64_t)per_sm * idx->num_sms < (int64_t)B * ch) return false;
     p = K6Plan{};
     p.resident = 1;
-    p.solo = solo ? 1 : 0;
+    p.cl = cl;
     p.G = G;
     p.gridsync = 1;
     p.chunks = (int)ch;
@@ -724,8 +779,8 @@ void launch_k7_resident(const pq_index_s* idx, const K6Plan& p, const float* phi
     a.id_base = (uint32_t)idx->id_base;
     a.chunks = p.chunks;
     a.chunk_items = (int)p.chunk_items;
-    a.solo = p.solo;
-    if (!p.solo) {
+    a.cl = p.cl;
+    if (!p.cl) {
         k7_reset<<<1, 256, 0, st>>>(reinterpret_cast<uint4*>(w), (int)(rb / 16));
         count_launch();
         check_launch("k7_reset");
@@ -736,19 +791,26 @@ void launch_k7_resident(const pq_index_s* idx, const K6Plan& p, const float* phi
     cfg.blockDim = dim3(K7_THREADS);
     cfg.dynamicSmemBytes = p.smem;
     cfg.stream = st;
-    // CTAs that poll each other's sub-id scores must be co-resident: a cooperative
-    // launch; solo CTAs never wait on each other (measured: neither attribute
-    // changes the C1 / C2a step)
+    // grid mode: CTAs that poll each other's sub-id scores must be co-resident (a
+    // cooperative launch); cluster mode: a cluster of cl CTAs per user
+    cudaLaunchAttribute at3[3];
+    (void)at;
     int na = 0;
-    if (!p.solo) {
-        at[na].id = cudaLaunchAttributeCooperative;
-        at[na].val.cooperative = 1;
+    if (!p.cl) {
+        at3[na].id = cudaLaunchAttributeCooperative;
+        at3[na].val.cooperative = 1;
+        ++na;
+    } else if (p.cl > 1) {
+        at3[na].id = cudaLaunchAttributeClusterDimension;
+        at3[na].val.clusterDim.x = (unsigned)p.cl;
+        at3[na].val.clusterDim.y = 1;
+        at3[na].val.clusterDim.z = 1;
         ++na;
     }
-    at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;   // after k7_reset / the producer of phi
-    at[na].val.programmaticStreamSerializationAllowed = 1;
+    at3[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;   // after k7_reset / the producer of phi
+    at3[na].val.programmaticStreamSerializationAllowed = 1;
     ++na;
-    cfg.attrs = at;
+    cfg.attrs = at3;
     cfg.numAttrs = na;
     const char* tf = getenv("PQTOPK_K6_TRACE");
     if (tf && *tf) {

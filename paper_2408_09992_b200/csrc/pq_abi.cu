@@ -612,7 +612,9 @@ pq_status pq_search_plan_info(pq_index idx, int32_t B, int32_t d, int32_t K, int
     need(d >= idx->m && d % idx->m == 0, "d must be a positive multiple of m");
     K6Plan kp;
     if (use_k6(idx, B, d, K, 0, kp)) {
-        out[0] = kp.resident ? 7 : 5; out[1] = kp.G; out[2] = kp.gridsync ? 0 : kp.CL; out[3] = 8;
+        out[0] = kp.resident ? 7 : 5; out[1] = kp.G;
+        out[2] = kp.resident ? kp.cl : (kp.gridsync ? 0 : kp.CL);
+        out[3] = kp.resident ? 16 : 8;
         out[4] = kp.grid; out[5] = kp.chunks; out[6] = 0; out[7] = (int64_t)kp.smem;
     } else {
         K2Plan p = plan_k2(idx, B, K);

@@ -183,7 +183,7 @@ struct K6Plan {
     int G = 0, nst = 0, CL = 0, chunks = 0, grid = 0;
     int gridsync = 0;             // 1: cooperative grid mode (S shared through L2), else clusters of CL
     int resident = 0;             // 1: K7 (k7_resident.cu): each CTA's code chunk resident in smem
-    int solo = 0;                 // K7 with one CTA per user (no exchange, no reset kernel, no ticket)
+    int cl = 0;                   // K7 cluster mode: one cluster of cl CTAs per user (no global exchange)
     int paired = 0;               // 1: the colour-paired row-order codes (idx->d_codes_p) with 16 table copies
     int64_t chunk_items = 0;
     size_t smem = 0, cand_bytes = 0;

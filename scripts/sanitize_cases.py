@@ -16,6 +16,7 @@ checked library).  Cases (SURVEY.md §5 "race detection"):
   k6clus    K6 fused query, cluster mode (cluster = 2)
   k6pair    K6 on the colour-paired row-order codes (a long stream: 10M items)
   k7        K7 fused query, chunk-resident codes (B = 1 and B = 2)
+  k7clus    K7 cluster mode (one 8-CTA cluster per user, sub-id scores and lists through DSMEM)
   merge     K3 pq_merge_topk over 8 shards
   subset    K5 subset V + exclusion lists
   recjpq    Alg. 2 on the GPU
@@ -103,6 +104,15 @@ def main(cases):
                 i, s = pq.pq_search(idx, cu(F), cu(P), 10, S_out=S)
                 torch.cuda.synchronize()
                 same(i.cpu().numpy(), s.cpu().numpy(), *oracle.pq_topk(G, S.cpu().numpy(), 10), c)
+        elif c == "k7clus":
+            G, P, F = pqsynth.random_instance(9014, 20_011, 8, 256, 64, 2)
+            idx = pq.pq_create(G, b=256)
+            pl = idx.search_plan(2, 64, 10)
+            assert pl["variant"] == 7 and pl["cluster"] == 8, pl
+            S = torch.empty((2, 8, 256), dtype=torch.float32, device=dev)
+            i, s = pq.pq_search(idx, cu(F), cu(P), 10, S_out=S)
+            torch.cuda.synchronize()
+            same(i.cpu().numpy(), s.cpu().numpy(), *oracle.pq_topk(G, S.cpu().numpy(), 10), c)
         elif c == "merge":
             G, P, F = pqsynth.random_instance(9006, 16_001, 4, 16, 16, 3)
             S = pq.pq_subscores(cu(F), cu(P))
@@ -149,7 +159,7 @@ if __name__ == "__main__":
     reps = 1
     if argv[:1] == ["--reps"]:
         reps, argv = int(argv[1]), argv[2:]
-    cases = argv or ["tiled16", "tiled8", "tiled4", "latency", "k6grid", "k6clus", "k6pair", "k7", "merge",
+    cases = argv or ["tiled16", "tiled8", "tiled4", "latency", "k6grid", "k6clus", "k6pair", "k7", "k7clus", "merge",
                      "subset", "recjpq", "dense"]
     import paper_2408_09992_b200 as _pq
     print("library:", _pq.lib_path(), flush=True)

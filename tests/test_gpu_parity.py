@@ -433,6 +433,8 @@ FUSED_CASES = [
     (534, 300_000, 8, 256, 64, 4, 30, "few"),          # 4 users, heavy ties
     (535, 100_000, 4, 16, 64, 1, 300, "uniform"),      # K = 300 ties: radix-selected floor / cuts
     (536, 10_000_019, 8, 256, 64, 2, 50, "zipf"),      # K6 on colour-paired rows (long stream), skewed codes
+    (537, 60_000, 8, 256, 64, 3, 20, "few"),           # K7 cluster mode: 3 users x 8-CTA clusters, ties
+    (538, 30_001, 4, 256, 32, 2, 64, "zipf"),          # K7 cluster mode, m = 4, 4-CTA clusters (cl * K <= 256)
 ]
 
 
