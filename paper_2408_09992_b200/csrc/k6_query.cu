@@ -56,7 +56,19 @@ struct K6Args {
 };
 
 constexpr int K6_THREADS = 256;
-constexpr int K6_STAGE = 16384;                    // code bytes per round (one TMA stage)
+// Round size: 24 KB of codes (3072 items at m = 8, 12 per thread) -- twice the
+// independent add chains of the 16 KB rounds and a third fewer rounds: c7
+// 2.38 -> 2.05 ms (32 KB rounds leave room for only two stages and measured
+// 3.37 ms).  A multiple of 8 KB, so every m in {4, 8, 16} gets an even J.
+#ifndef K6_STAGE_BYTES
+#define K6_STAGE_BYTES 24576
+#endif
+#ifndef K6_CAP_SLACK
+#define K6_CAP_SLACK 512                               // 0: candidate buffer of 2 rounds of items
+#endif
+constexpr int K6_STAGE = K6_STAGE_BYTES;               // code bytes per round (one TMA stage)
+// candidate buffer: one round of items + room for the K kept ones (K <= 512)
+__host__ __device__ constexpr int k6_cap(int ipr) { return K6_CAP_SLACK ? ipr + K6_CAP_SLACK : 2 * ipr; }
 
 // Bitonic sort of one key per lane across a warp, descending (lane 0 = largest).
 __device__ __forceinline__ uint64_t warp_sort32_desc(uint64_t v) {
@@ -110,7 +122,7 @@ __global__ void __launch_bounds__(K6_THREADS) k6_query(const K6Args a) {
     constexpr int NW = MP / 4;
     constexpr int IPR = K6_STAGE / MP;                // items per round
     constexpr int J = IPR / K6_THREADS;
-    constexpr int CAP = 2 * IPR;
+    constexpr int CAP = k6_cap(IPR);
     constexpr int NWARP = K6_THREADS / 32;
     extern __shared__ __align__(128) unsigned char sm_raw[];
     const int bq = BB > 0 ? BB : a.b;                 // sub-ids per split
@@ -724,7 +736,7 @@ static K6Fn query_fn(int m, int G, int b) {
     }
 }
 static int query_mp(int m) { return (m + 3) / 4 * 4; }
-static int query_cap(int m) { return 2 * (K6_STAGE / query_mp(m)); }
+static int query_cap(int m) { return k6_cap(K6_STAGE / query_mp(m)); }
 static size_t query_smem(int m, int b, int G, int nst, int d, int B) {
     return align_up((size_t)m * b * G * 4, 128) + (size_t)nst * K6_STAGE + k6_pro_bytes(query_cap(m), d, m * b, B) +
            256 * 4;
