@@ -73,6 +73,14 @@ namespace pq {
 #endif
 int k2_tiled_code_bytes() { return K2_CODE_BYTES; }
 
+// Union floors (large K): a finished unit publishes, per user, the keys of rank
+// ceil(K / c) of its list for c = 2, 4, 8, 16 (K2_NQ levels).  If c finished
+// units of a user each published a level-c key >= v, then c * ceil(K / c) >= K
+// distinct items (the chunks are disjoint) have keys >= v, so v is a proved
+// floor for that user's top-K (like gtau, which is the c = 1 level).  A unit
+// starting later takes the largest such v over the levels: after j finished
+// chunks it admits ~K / j items per user instead of ~K (C5: K = 1000).
+constexpr int K2_NQ = 4;
 struct K2TArgs {
     const void* codes;         // phase-blocked codes (see above), K2_CODE_BYTES each
     int64_t codes_bytes;       // allocated bytes of `codes` (checked builds bound every load)
@@ -88,6 +96,8 @@ struct K2TArgs {
     int wm;                    // shrink watermark (<= cap - (2 slack + 1) TR - 32)
     uint64_t* cand;            // [B][chunks][K]
     unsigned long long* gtau;  // [n_groups * R] per-user proved thresholds (zeroed per call)
+    unsigned long long* qk;    // [n_groups * R][chunks][K2_NQ] union-floor keys (zeroed per call), or null
+    int32_t* lcnt;             // [n_groups * R][chunks] entries of each unit's list in cand (no padding)
     long long* trace;          // diagnostics (PQTOPK_K2_TRACE): CTA 0 phase timeline, or null
     int trace_stride;          // trace every trace_stride-th tile (PQTOPK_K2_TRACE_STRIDE)
     int trace_from;            // first traced tile of CTA 0 (PQTOPK_K2_TRACE_FROM)
@@ -489,6 +499,46 @@ __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
         if (threadIdx.x < n_valid)                                // K keys >= gtau exist elsewhere
             tau_sh[threadIdx.x] = *reinterpret_cast<volatile unsigned long long*>(&gtau_g[threadIdx.x]);
         __syncthreads();
+        if (a.qk) {                                               // union floors (chunks <= 64)
+            for (int u = warp; u < n_valid; u += W) {
+                const volatile unsigned long long* qu = a.qk + (int64_t)(grp * R + u) * a.chunks * K2_NQ;
+                uint64_t v[2][K2_NQ];
+#pragma unroll
+                for (int i = 0; i < 2; ++i) {
+                    const int ch = lane + 32 * i;
+#pragma unroll
+                    for (int l = 0; l < K2_NQ; ++l) v[i][l] = ch < a.chunks ? qu[ch * K2_NQ + l] : 0ull;
+                }
+                int c_ge[2][K2_NQ] = {};                          // published keys >= mine, per level
+#pragma unroll 4
+                for (int j = 0; j < 32; ++j) {
+#pragma unroll
+                    for (int i2 = 0; i2 < 2; ++i2)
+#pragma unroll
+                        for (int l = 0; l < K2_NQ; ++l) {
+                            const uint64_t w = __shfl_sync(FULL, v[i2][l], j);
+#pragma unroll
+                            for (int i = 0; i < 2; ++i) c_ge[i][l] += w >= v[i][l];
+                        }
+                }
+                uint64_t fl = 0ull;
+#pragma unroll
+                for (int i = 0; i < 2; ++i)
+#pragma unroll
+                    for (int l = 0; l < K2_NQ; ++l)
+                        if (v[i][l] != 0ull && c_ge[i][l] >= (2 << l) && v[i][l] > fl) fl = v[i][l];
+#pragma unroll
+                for (int o = 16; o; o >>= 1) {
+                    const uint64_t t = __shfl_xor_sync(FULL, fl, o);
+                    fl = t > fl ? t : fl;
+                }
+                if (lane == 0 && fl != 0ull) {
+                    atomicMax(&tau_sh[u], (unsigned long long)fl);
+                    atomicMax(&gtau_g[u], (unsigned long long)fl);
+                }
+            }
+            __syncthreads();
+        }
         float tf[4];
 #pragma unroll
         for (int j = 0; j < 4; ++j)
@@ -791,7 +841,22 @@ __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
             const uint64_t kth = shrink_user(ub, nconv_u[u], cnt_u[u], a.K, tau_sh[u], out, hist,
                                              a.perm, a.id_base, nn);
             if (lane == 0 && kth) atomicMax(&gtau_g[u], (unsigned long long)kth);
-            for (int j = nn + lane; j < a.K; j += 32) out[j] = 0ull;
+            if (a.lcnt) {                                  // K3 reads nn entries: no padding
+                if (lane == 0) a.lcnt[(int64_t)gu * a.chunks + chunk] = nn;
+            } else {
+                for (int j = nn + lane; j < a.K; j += 32) out[j] = 0ull;
+            }
+            if (a.qk) {                                    // publish this chunk's union-floor keys
+                __syncwarp();                              // the list written by every lane
+                volatile unsigned long long* qo = a.qk + ((int64_t)gu * a.chunks + chunk) * K2_NQ;
+#pragma unroll 1
+                for (int l = 0; l < K2_NQ; ++l) {
+                    const int r = (a.K + (2 << l) - 1) / (2 << l);
+                    const uint64_t key = nn >= r ? warp_kth(out, nn, (uint32_t)r, hist) : 0ull;
+                    if (lane == 0) qo[l] = key;
+                    __syncwarp();
+                }
+            }
         }
         __syncthreads();
         if (threadIdx.x < R) { tau_sh[threadIdx.x] = 0ull; cnt_u[threadIdx.x] = 0; nconv_u[threadIdx.x] = 0; }
@@ -824,11 +889,11 @@ __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
 // interleaved table layout (colour-renumbered for R = 16), so K2 can stage a
 // phase's tables with one contiguous bulk copy.
 __global__ void k2_tile_S(const float* __restrict__ S, const uint8_t* __restrict__ cmap, int B, int m,
-                          int b, int R, int n_groups, float* __restrict__ St, unsigned long long* gtau) {
+                          int b, int R, int n_groups, float* __restrict__ St, unsigned long long* gtau, int64_t nz) {
     pdl_wait();                                        // S comes from K1
     pdl_trigger();
-    for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < n_groups * R; x += gridDim.x * blockDim.x)
-        gtau[x] = 0ull;                                // the call's shared thresholds start unset
+    for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < nz; x += (int64_t)gridDim.x * blockDim.x)
+        gtau[x] = 0ull;                                // the call's shared thresholds (+ union floors) start unset
     const int64_t total = (int64_t)n_groups * m * b * R;
     for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < total;
          x += (int64_t)gridDim.x * blockDim.x) {
@@ -849,11 +914,11 @@ __global__ void k2_tile_S(const float* __restrict__ S, const uint8_t* __restrict
 // (the first partial sum of Eq. 5 in the sequential order), then 16 rows per
 // remaining split k = 2 .. m-1.
 __global__ void k2_tile_S_pair(const float* __restrict__ S, int B, int m, int R, int n_groups,
-                               float* __restrict__ St, unsigned long long* gtau) {
+                               float* __restrict__ St, unsigned long long* gtau, int64_t nz) {
     pdl_wait();                                        // S comes from K1
     pdl_trigger();
-    for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < n_groups * R; x += gridDim.x * blockDim.x)
-        gtau[x] = 0ull;                                // the call's shared thresholds start unset
+    for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < nz; x += (int64_t)gridDim.x * blockDim.x)
+        gtau[x] = 0ull;                                // the call's shared thresholds (+ union floors) start unset
     const int rows = 256 + (m - 2) * 16;
     const int64_t total = (int64_t)n_groups * rows * R;
     for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < total;
@@ -944,6 +1009,7 @@ size_t k2_tiled_smem(const TiledShape& t, int W) {
     return align_up(base, 16) + lm + 16;
 }
 static int k2_slack() { return K2_SLACK; }
+static int64_t qk_words(const K2Plan& p) { return p.qk ? (int64_t)p.n_groups * p.G * p.chunks * K2_NQ : 0; }
 static size_t st_table_bytes(const TiledShape& t, int n_groups) {
     return (size_t)n_groups * (t.bt0 + (t.m_v - 1) * t.bt) * t.R * 4;
 }
@@ -1006,12 +1072,26 @@ void plan_k2_tiled(const pq_index_s* idx, int B, int K, K2Plan& p) {
     p.lanebuf_bytes = (size_t)p.grid * R * p.cap * 8;
     p.cand_bytes = (size_t)B * p.chunks * K * 8;
     p.mscr_bytes = 0;
-    p.st_bytes = align_up(st_table_bytes(sh, p.n_groups), 256) + (size_t)p.n_groups * R * 8;
+    // union floors (K2_NQ levels per finished unit) for large K on single-phase tables:
+    // each unit otherwise admits ~K items per user (C5: K = 1000, 37 chunks; K2 DRAM
+    // bytes 8.2 -> 4.3 GB, time -0.5%).  Not for K = 100 (C3: the unit-end level
+    // selections cost 1.4% and save 10% of a small traffic)
+    static const char* qe = getenv("PQTOPK_K2_UNION");   // A/B: 0 = off
+    p.qk = (sh.m_v / sh.ps) == 1 && K >= 256 && p.chunks >= 3 && p.chunks <= 64 && !(qe && *qe == '0');
+    p.st_bytes = align_up(st_table_bytes(sh, p.n_groups), 256) + (size_t)p.n_groups * R * 8 +
+                 (size_t)qk_words(p) * 8 + (size_t)p.n_groups * R * p.chunks * 4;
 }
 
+// St workspace: [tables][gtau: n_groups R u64][qk: n_groups R chunks K2_NQ u64 when p.qk][lcnt: n_groups R chunks i32]
 static unsigned long long* gtau_of(const pq_index_s* idx, const K2Plan& p, const float* St) {
     return reinterpret_cast<unsigned long long*>(const_cast<char*>(reinterpret_cast<const char*>(St)) +
                                                  align_up(st_table_bytes(k2_tiled_shape(idx->m, idx->b), p.n_groups), 256));
+}
+static unsigned long long* qk_of(const pq_index_s* idx, const K2Plan& p, const float* St) {
+    return p.qk ? gtau_of(idx, p, St) + (int64_t)p.n_groups * p.G : nullptr;
+}
+const int32_t* k2_tiled_list_counts(const pq_index_s* idx, const K2Plan& p, const float* St) {
+    return reinterpret_cast<const int32_t*>(gtau_of(idx, p, St) + (int64_t)p.n_groups * p.G + qk_words(p));
 }
 
 void launch_k2_tiled_prep(const pq_index_s* idx, const K2Plan& p, const float* S, int B, float* St,
@@ -1022,9 +1102,10 @@ void launch_k2_tiled_prep(const pq_index_s* idx, const K2Plan& p, const float* S
     const int threads = 256;
     const int blocks = (int)std::min<int64_t>(ceil_div(total, threads), (int64_t)idx->num_sms * 16);
     unsigned long long* gtau = gtau_of(idx, p, St);
-    if (sh.pair) launch_pdl(k2_tile_S_pair, dim3(blocks), dim3(threads), 0, st, S, B, idx->m, p.G, p.n_groups, St, gtau);
+    const int64_t nz = (int64_t)p.n_groups * p.G + qk_words(p);
+    if (sh.pair) launch_pdl(k2_tile_S_pair, dim3(blocks), dim3(threads), 0, st, S, B, idx->m, p.G, p.n_groups, St, gtau, nz);
     else launch_pdl(k2_tile_S, dim3(blocks), dim3(threads), 0, st, S, (const uint8_t*)idx->d_cmap3, B, idx->m, idx->b, p.G,
-                    p.n_groups, St, gtau);
+                    p.n_groups, St, gtau, nz);
     count_launch();
     check_launch("k2_tile_S");
 }
@@ -1049,6 +1130,8 @@ void launch_k2_tiled(const pq_index_s* idx, const K2Plan& p, int B, int K,
         a.wm = tw > 0 ? std::min(std::max(tw, K + 1), wmax) : wmax;
     }
     a.gtau = gtau_of(idx, p, St);
+    a.qk = qk_of(idx, p, St);
+    a.lcnt = const_cast<int32_t*>(k2_tiled_list_counts(idx, p, St));
     const char* dbe = getenv("PQTOPK_K2_DEBUG");
     if (dbe && *dbe) {
         PQ_CUDA(cudaMalloc(&a.dbg, 64 * 4));

@@ -20,6 +20,16 @@ struct SrcKeys {        // keys[u][e], row length L
     int64_t L;
     __device__ __forceinline__ uint64_t get(int u, int64_t e) const { return keys[(int64_t)u * L + e]; }
 };
+struct SrcKeysCnt {     // keys[u][e], e = p*K + j: lists of K keys, lcnt[u][p] of them written
+    const uint64_t* keys;
+    int64_t L;
+    const int32_t* lcnt;
+    int K, P;
+    __device__ __forceinline__ uint64_t get(int u, int64_t e) const {
+        const int p = (int)((uint32_t)e / (uint32_t)K), j = (int)(e - (int64_t)p * K);   // e < P * K < 2^32
+        return j < __ldg(&lcnt[(int64_t)u * P + p]) ? keys[(int64_t)u * L + e] : 0ull;
+    }
+};
 struct SrcPairs {       // (ids, scores)[p][u][j] at p*pstride + u*K + j, e = p*K + j
     const int32_t* ids;
     const float* sc;
@@ -167,7 +177,7 @@ size_t k3_reduce_scratch_bytes(int64_t L, int B, int K) {
 }
 
 void k3_keys_to_topk(const uint64_t* keys, int64_t L, int B, int K, void* scratch,
-                     int32_t* ids, float* scores, cudaStream_t st) {
+                     int32_t* ids, float* scores, cudaStream_t st, const int32_t* lcnt) {
     if (B <= 0 || K <= 0) return;
     const uint64_t* cur = keys;
     int64_t curL = L;
@@ -175,6 +185,18 @@ void k3_keys_to_topk(const uint64_t* keys, int64_t L, int B, int K, void* scratc
     uint64_t* bufs[2] = {reinterpret_cast<uint64_t*>(scratch),
                          reinterpret_cast<uint64_t*>(reinterpret_cast<char*>(scratch) + half)};
     int pp = 0;
+    if (lcnt) {                                        // first level reads the counted lists
+        const SrcKeysCnt src{keys, L, lcnt, K, (int)(L / K)};
+        if (L <= K3_SEG) {
+            launch_k3(src, L, B, K, nullptr, 0, 0, ids, scores, st);
+            return;
+        }
+        const int64_t n_sub = ceil_div(L, K3_SEG);
+        launch_k3(src, L, B, K, bufs[pp], n_sub, 0, nullptr, nullptr, st);
+        cur = bufs[pp];
+        curL = n_sub * K;
+        pp ^= 1;
+    }
     while (curL > K3_SEG) {
         int64_t n_sub = ceil_div(curL, K3_SEG);
         uint64_t* out = bufs[pp];

@@ -108,7 +108,8 @@ static void run_score_topk(pq_index_s* idx, const float* S, int B, int K, void* 
     else if (w.plan.variant == 4) launch_k2_latency(idx, w.plan, S, B, K, cand, st);
     else launch_k2(idx, w.plan, S, B, K, lanebuf, cand, st);
     if (idx->timing) PQ_CUDA(cudaEventRecord(ev.b, st));
-    k3_keys_to_topk(cand, (int64_t)w.plan.chunks * K, B, K, k3s, ids, scores, st);
+    k3_keys_to_topk(cand, (int64_t)w.plan.chunks * K, B, K, k3s, ids, scores, st,
+                    w.plan.variant == 3 ? k2_tiled_list_counts(idx, w.plan, St) : nullptr);
     if (idx->timing) {
         PQ_CUDA(cudaEventRecord(ev.c, st));
         std::lock_guard<std::mutex> lk(*idx->ev_mu);

@@ -176,7 +176,8 @@ struct K2Plan {
     size_t mscr_bytes = 0;        // grid * 32 * W * K * 8 (end-of-unit merge scratch)
     int variant = 1;
     int tm = 0;
-    size_t st_bytes = 0;          // v3: tiled S tables [n_groups][m][b][16] fp32
+    size_t st_bytes = 0;          // v3: tiled S tables [n_groups][m][b][16] fp32 + thresholds, union floors, list counts
+    bool qk = false;              // v3: union floors (large K, single-phase tables)
 };
 // K6 (k6_query.cu): the fused single-launch query kernel for B <= 4
 struct K6Plan {
@@ -223,6 +224,8 @@ void launch_k2_tiled_prep(const pq_index_s* idx, const K2Plan& p, const float* S
                           cudaStream_t st);
 void launch_k2_tiled(const pq_index_s* idx, const K2Plan& p, int B, int K,
                      uint64_t* lanebuf, uint64_t* mscr, const float* St, uint64_t* cand, cudaStream_t st);
+// v3 writes each unit's list unpadded: entries per (user, chunk) list, [n_groups R][chunks]
+const int32_t* k2_tiled_list_counts(const pq_index_s* idx, const K2Plan& p, const float* St);
 K2Plan plan_k2(const pq_index_s* idx, int B, int K);
 void launch_k2(const pq_index_s* idx, const K2Plan& p, const float* S, int B, int K,
                uint64_t* lanebuf, uint64_t* cand, cudaStream_t st);
@@ -231,8 +234,9 @@ void launch_k2(const pq_index_s* idx, const K2Plan& p, const float* S, int B, in
 constexpr int K3_SEG = 8192;           // keys per K3 block (smem-resident; 2 blocks per SM; >= 2 PQTOPK_MAX_K so every merge level halves the list)
 size_t k3_reduce_scratch_bytes(int64_t L, int B, int K);
 // keys [B][L] -> ids/scores [B][K] (sorted), multi-level; scratch from above
+// lcnt (optional): keys[u] is lists of K keys of which lcnt[u * L / K + p] are valid (the rest unwritten)
 void k3_keys_to_topk(const uint64_t* keys, int64_t L, int B, int K, void* scratch,
-                     int32_t* ids, float* scores, cudaStream_t st);
+                     int32_t* ids, float* scores, cudaStream_t st, const int32_t* lcnt = nullptr);
 // pairs [P][B][K] -> ids/scores [B][K]
 size_t k3_pairs_scratch_bytes(int P, int B, int K);
 void k3_pairs_to_topk(const int32_t* ids_in, const float* sc_in, int64_t pstride, int P, int B,
