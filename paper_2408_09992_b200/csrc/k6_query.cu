@@ -55,7 +55,10 @@ struct K6Args {
     long long* trace;          // diagnostics (PQTOPK_K6_TRACE): [grid][32] globaltimer stamps, or null
 };
 
-constexpr int K6_THREADS = 256;
+#ifndef K6_THREADS_N
+#define K6_THREADS_N 256
+#endif
+constexpr int K6_THREADS = K6_THREADS_N;
 // Round size: 24 KB of codes (3072 items at m = 8, 12 per thread) -- twice the
 // independent add chains of the 16 KB rounds and a third fewer rounds: c7
 // 2.38 -> 2.05 ms (32 KB rounds leave room for only two stages and measured

@@ -386,6 +386,24 @@ def test_tiled_parity(pq, torch, orc, case):
         assert_same(i.cpu().numpy(), s.cpu().numpy(), *ref, str(tun))
 
 
+@pytest.mark.parametrize("dist,chunks", [("uniform", 37), ("few", 11)])
+def test_union_floors_many_chunks(pq, torch, orc, dist, chunks):
+    """Union floors (K >= 256, single-phase tables, 3..64 chunks): a unit starts
+    from the largest key that c finished chunks of the user vouch for with their
+    rank-ceil(K/c) keys, and writes its list unpadded (K3 reads per-list
+    counts).  C5-shaped (m = 4, b = 16: exact score ties across tuples), many
+    chunks per user, bit-exact against the oracle."""
+    G, P, F = pqsynth.random_instance(313, 1_200_007, 4, 16, 16, 70, code_dist=dist)
+    idx = pq.pq_create(G, b=16, id_base=5)
+    S_t = pq.pq_subscores(cuda(torch, F), cuda(torch, P))
+    ref = orc.pq_topk(G, S_t.cpu().numpy(), 1000, id_base=5)
+    for tun in (dict(variant=3, chunks=chunks), dict(variant=3, chunks=chunks, ctas=9)):
+        idx.set_tuning(**tun)
+        assert idx.plan(70, 1000)["chunks"] == chunks
+        i, s = pq.pq_score_topk(idx, S_t, 1000)
+        assert_same(i.cpu().numpy(), s.cpu().numpy(), *ref, str(tun))
+
+
 LATENCY_CASES = [
     # seed, N, m, b, B, K, dist — the serving case (B <= 4; SURVEY §8(f) f4)
     (500, 10_000, 8, 256, 1, 10, "uniform"),        # C1 shape
