@@ -135,6 +135,12 @@ __device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sy
 __device__ __forceinline__ float4 lds128(const char* p) {
     return *reinterpret_cast<const float4*>(p);
 }
+// the same load from a 32-bit shared address plus a compile-time offset
+__device__ __forceinline__ float4 lds128_s(uint32_t addr, uint32_t imm) {
+    float4 v;
+    asm("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr + imm));
+    return v;
+}
 // 4 users' running sums += 4 sub-scores (two packed fp32x2 adds, RN, no FTZ)
 __device__ __forceinline__ void add4(float4& acc, const float4 v) {
     float2 lo = __fadd2_rn(make_float2(acc.x, acc.y), make_float2(v.x, v.y));
@@ -178,7 +184,11 @@ template <int PS> struct CodePair {
     __device__ __forceinline__ uint32_t off(int e, int kk, uint32_t q16) const {
         if constexpr (K2_CODE_BYTES == 1) {
             const uint32_t wd = w[(e * PS + kk) >> 2];     // PS here = stored codes per row
+#ifndef K2_NO_ASM_LDS
+            if constexpr (true)                            // PRMT + one IMAD (code * RB + base) per gather
+#else
             if constexpr (PS == 4)                         // byte extract by PRMT (C4: -0.6%)
+#endif
                 return __byte_perm(wd, 0u, 0x4440u | (uint32_t)((e * PS + kk) & 3)) * RB + q16;
             else
                 return ((wd >> (8 * ((e * PS + kk) & 3))) & 0xFFu) * RB + q16;
@@ -339,11 +349,73 @@ __device__ __noinline__ uint64_t shrink_user(uint64_t* ub, int nc, int n, int K,
     return kth;
 }
 
+// Union floors at a unit's start (see K2_NQ): warp w takes users w, w + W, ...;
+// lane l holds chunks l and l + 32 of the user's published keys.  Out of line so
+// that its registers do not shape the scoring loop's allocation.
+template <int W>
+__device__ __noinline__ void union_floors(const volatile unsigned long long* qg, int chunks, int n_valid,
+                                          unsigned long long* tau_sh, unsigned long long* gtau_g) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int u = warp; u < n_valid; u += W) {
+        const volatile unsigned long long* qu = qg + (int64_t)u * chunks * K2_NQ;
+        uint64_t v[2][K2_NQ];
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+            const int ch = lane + 32 * i;
+#pragma unroll
+            for (int l = 0; l < K2_NQ; ++l) v[i][l] = ch < chunks ? qu[ch * K2_NQ + l] : 0ull;
+        }
+        int c_ge[2][K2_NQ] = {};                          // published keys >= mine, per level
+#pragma unroll 4
+        for (int j = 0; j < 32; ++j) {
+#pragma unroll
+            for (int i2 = 0; i2 < 2; ++i2)
+#pragma unroll
+                for (int l = 0; l < K2_NQ; ++l) {
+                    const uint64_t w = __shfl_sync(FULL, v[i2][l], j);
+#pragma unroll
+                    for (int i = 0; i < 2; ++i) c_ge[i][l] += w >= v[i][l];
+                }
+        }
+        uint64_t fl = 0ull;
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+#pragma unroll
+            for (int l = 0; l < K2_NQ; ++l)
+                if (v[i][l] != 0ull && c_ge[i][l] >= (2 << l) && v[i][l] > fl) fl = v[i][l];
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+            const uint64_t t = __shfl_xor_sync(FULL, fl, o);
+            fl = t > fl ? t : fl;
+        }
+        if (lane == 0 && fl != 0ull) {
+            atomicMax(&tau_sh[u], (unsigned long long)fl);
+            atomicMax(&gtau_g[u], (unsigned long long)fl);
+        }
+    }
+}
+
+// A finished unit's list -> its K2_NQ union-floor keys (one warp; out of line).
+__device__ __noinline__ void union_publish(volatile unsigned long long* qo, const uint64_t* out, int nn, int K,
+                                           uint32_t* hist) {
+    const int lane = threadIdx.x & 31;
+    __syncwarp();                                      // the list written by every lane
+#pragma unroll 1
+    for (int l = 0; l < K2_NQ; ++l) {
+        const int r = (K + (2 << l) - 1) / (2 << l);
+        const uint64_t key = nn >= r ? warp_kth(out, nn, (uint32_t)r, hist) : 0ull;
+        if (lane == 0) qo[l] = key;
+        __syncwarp();
+    }
+}
+
 // ---------------------------------------------------------------- the kernel
 // M splits, PS per phase (NP = M / PS phases), BT sub-ids, R users per table
 // row, W warps, D slots of code prefetch, BT0 rows in split 0's table (BT0 !=
 // BT: the exact first-pair table, single-phase only — see below).
-template <int M, int PS, int BT, int R, int W, int D, int BT0 = BT>
+// UQ: union floors (K2_NQ) compiled in -- a separate instantiation, selected by the
+// planner for large K, so the other configurations' kernels do not carry its code.
+template <int M, int PS, int BT, int R, int W, int D, int BT0 = BT, bool UQ = false>
 __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
     constexpr int NP = M / PS;
     // table buffers: NP == 1: one; NP > 1: a 2-slot ring (buffers 0, 1) for phases
@@ -499,44 +571,8 @@ __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
         if (threadIdx.x < n_valid)                                // K keys >= gtau exist elsewhere
             tau_sh[threadIdx.x] = *reinterpret_cast<volatile unsigned long long*>(&gtau_g[threadIdx.x]);
         __syncthreads();
-        if (a.qk) {                                               // union floors (chunks <= 64)
-            for (int u = warp; u < n_valid; u += W) {
-                const volatile unsigned long long* qu = a.qk + (int64_t)(grp * R + u) * a.chunks * K2_NQ;
-                uint64_t v[2][K2_NQ];
-#pragma unroll
-                for (int i = 0; i < 2; ++i) {
-                    const int ch = lane + 32 * i;
-#pragma unroll
-                    for (int l = 0; l < K2_NQ; ++l) v[i][l] = ch < a.chunks ? qu[ch * K2_NQ + l] : 0ull;
-                }
-                int c_ge[2][K2_NQ] = {};                          // published keys >= mine, per level
-#pragma unroll 4
-                for (int j = 0; j < 32; ++j) {
-#pragma unroll
-                    for (int i2 = 0; i2 < 2; ++i2)
-#pragma unroll
-                        for (int l = 0; l < K2_NQ; ++l) {
-                            const uint64_t w = __shfl_sync(FULL, v[i2][l], j);
-#pragma unroll
-                            for (int i = 0; i < 2; ++i) c_ge[i][l] += w >= v[i][l];
-                        }
-                }
-                uint64_t fl = 0ull;
-#pragma unroll
-                for (int i = 0; i < 2; ++i)
-#pragma unroll
-                    for (int l = 0; l < K2_NQ; ++l)
-                        if (v[i][l] != 0ull && c_ge[i][l] >= (2 << l) && v[i][l] > fl) fl = v[i][l];
-#pragma unroll
-                for (int o = 16; o; o >>= 1) {
-                    const uint64_t t = __shfl_xor_sync(FULL, fl, o);
-                    fl = t > fl ? t : fl;
-                }
-                if (lane == 0 && fl != 0ull) {
-                    atomicMax(&tau_sh[u], (unsigned long long)fl);
-                    atomicMax(&gtau_g[u], (unsigned long long)fl);
-                }
-            }
+        if constexpr (UQ) {                                       // union floors (chunks <= 64)
+            union_floors<W>(a.qk + (int64_t)grp * R * a.chunks * K2_NQ, a.chunks, n_valid, tau_sh, gtau_g);
             __syncthreads();
         }
         float tf[4];
@@ -623,6 +659,10 @@ __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
                 mbar_wait(bar0 + 8u * buf, par);
                 if (trc) a.trace[((int64_t)warp * TRACE_PH + tix) * 3 + 1] = clock64();
                 const char* tb = reinterpret_cast<const char*>(sm_raw) + buf * TBLB;
+#ifndef K2_NO_ASM_LDS
+                uint32_t tbq32 = tbl0 + (uint32_t)buf * TBLB + q16;
+                asm volatile("" : "+r"(tbq32) :: "memory");   // defined after the wait: no gather moves above it
+#endif
                 const uint32_t row0 = (uint32_t)(tile * TR) + (uint32_t)(warp * SL * RPS) + (uint32_t)(lane / LPR);
                 // codes of this warp's slot pairs: [pair][row][2 slots][PS]
                 const char* cp = reinterpret_cast<const char*>(a.codes) + ((tile * NP + ph) * TR +
@@ -652,7 +692,13 @@ __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
 #pragma unroll
                         for (int kk = 0; kk < PS; ++kk) {
                             PQ_DCHECK(split_off(kk) + cw[d >> 1].template off<RB>(d & 1, kk, q16) + 16 <= TBLB);
+#ifndef K2_NO_ASM_LDS
+                            // 32-bit shared address = code * RB + (buffer + quad offset): ONE IMAD per
+                            // gather (with a generic pointer the compiler adds base and quad separately)
+                            dst[kk] = lds128_s(cw[d >> 1].template off<RB>(d & 1, kk, tbq32), split_off(kk));
+#else
                             dst[kk] = lds128(tb + split_off(kk) + cw[d >> 1].template off<RB>(d & 1, kk, q16));
+#endif
                         }
                         if (d & 1) {                   // both slots of the pair addressed: refill
                             CodePair<PSS>::check(cp, reinterpret_cast<const char*>(a.codes), a.codes_bytes);
@@ -846,17 +892,8 @@ __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
             } else {
                 for (int j = nn + lane; j < a.K; j += 32) out[j] = 0ull;
             }
-            if (a.qk) {                                    // publish this chunk's union-floor keys
-                __syncwarp();                              // the list written by every lane
-                volatile unsigned long long* qo = a.qk + ((int64_t)gu * a.chunks + chunk) * K2_NQ;
-#pragma unroll 1
-                for (int l = 0; l < K2_NQ; ++l) {
-                    const int r = (a.K + (2 << l) - 1) / (2 << l);
-                    const uint64_t key = nn >= r ? warp_kth(out, nn, (uint32_t)r, hist) : 0ull;
-                    if (lane == 0) qo[l] = key;
-                    __syncwarp();
-                }
-            }
+            if constexpr (UQ)                              // publish this chunk's union-floor keys
+                union_publish(a.qk + ((int64_t)gu * a.chunks + chunk) * K2_NQ, out, nn, a.K, hist);
         }
         __syncthreads();
         if (threadIdx.x < R) { tau_sh[threadIdx.x] = 0ull; cnt_u[threadIdx.x] = 0; nconv_u[threadIdx.x] = 0; }
@@ -943,8 +980,14 @@ __global__ void k2_tile_S_pair(const float* __restrict__ S, int B, int m, int R,
 typedef void (*K2TFn)(const K2TArgs);
 
 template <int M, int PS, int BT, int R, int BT0 = BT>
-static K2TFn tiled_fn_w(int W) {
+static K2TFn tiled_fn_w(int W, bool uq) {
     // deeper code prefetch for m = 16 (C4: -1.7 %; m = 8 and m = 64 prefer 4)
+    if constexpr (M == PS) {                           // single-phase tables: a union-floor variant
+        if (uq) {
+            if (W == 16) return k2_tiled<M, PS, BT, R, 16, 4, BT0, true>;
+            return k2_tiled<M, PS, BT, R, 8, 4, BT0, true>;
+        }
+    }
     if (W == 16) return k2_tiled<M, PS, BT, R, 16, (M == 16 ? 8 : 4), BT0>;
     return k2_tiled<M, PS, BT, R, 8, 4, BT0>;
 }
@@ -952,28 +995,28 @@ static K2TFn tiled_fn_w(int W) {
 // 256-row "split" whose row c = g0 + 16 g1 holds fl(S[0][g0] + S[1][g1]) -- the
 // first partial sum of Eq. 5 exactly as the sequential order computes it -- so
 // an item costs m - 1 lookups.
-static K2TFn tiled_pair_fn(int m_v, int W) {
-    if (m_v == 3) return tiled_fn_w<3, 3, 16, 32, 256>(W);
-    if (m_v == 7) return tiled_fn_w<7, 7, 16, 32, 256>(W);
+static K2TFn tiled_pair_fn(int m_v, int W, bool uq = false) {
+    if (m_v == 3) return tiled_fn_w<3, 3, 16, 32, 256>(W, uq);
+    if (m_v == 7) return tiled_fn_w<7, 7, 16, 32, 256>(W, uq);
     return nullptr;
 }
 // Instantiated shapes: R = 16 (paired layout) for b = 256, m in {8, 16, 32, 64};
 // R = 32 (item order) when the 32-user table fits: (m, b) in {(4, 16), (8, 16), (4, 256)}.
-static K2TFn tiled_fn(int m, int b, int R, int W) {
+static K2TFn tiled_fn(int m, int b, int R, int W, bool uq = false) {
     if (R == 16 && b == 256) {
-        if (m == 16) return tiled_fn_w<16, 4, 256, 16>(W);
-        if (m == 8) return tiled_fn_w<8, 8, 256, 16>(W);
+        if (m == 16) return tiled_fn_w<16, 4, 256, 16>(W, uq);
+        if (m == 8) return tiled_fn_w<8, 8, 256, 16>(W, uq);
     }
     if (R == 32 && b == 16) {
-        if (m == 4) return tiled_fn_w<4, 4, 16, 32>(W);
-        if (m == 8) return tiled_fn_w<8, 8, 16, 32>(W);
+        if (m == 4) return tiled_fn_w<4, 4, 16, 32>(W, uq);
+        if (m == 8) return tiled_fn_w<8, 8, 16, 32>(W, uq);
     }
-    if (R == 32 && b == 256 && m == 4) return tiled_fn_w<4, 4, 256, 32>(W);
+    if (R == 32 && b == 256 && m == 4) return tiled_fn_w<4, 4, 256, 32>(W, uq);
     // many splits (Fig. 2b's m = 64): 16 users, phases of 4 splits; pq_create pairs
     // items on complementary colours over the first 20 splits (64-split signatures
     // have no complements), so those splits' gathers are conflict-free
-    if (R == 16 && b == 256 && m == 32) return tiled_fn_w<32, 4, 256, 16>(W);
-    if (R == 16 && b == 256 && m == 64) return tiled_fn_w<64, 4, 256, 16>(W);
+    if (R == 16 && b == 256 && m == 32) return tiled_fn_w<32, 4, 256, 16>(W, uq);
+    if (R == 16 && b == 256 && m == 64) return tiled_fn_w<64, 4, 256, 16>(W, uq);
     return nullptr;
 }
 int k2_tiled_ps(int m) { return m >= 16 ? 4 : m; }
@@ -992,8 +1035,8 @@ TiledShape k2_tiled_shape(int m, int b) {
     t.pss = (t.ps == 3 || t.ps == 7) ? t.ps + 1 : t.ps;
     return t;
 }
-static K2TFn tiled_fn_shape(const TiledShape& t, int W) {
-    return t.pair ? tiled_pair_fn(t.m_v, W) : tiled_fn(t.m_v, t.bt, t.R, W);
+static K2TFn tiled_fn_shape(const TiledShape& t, int W, bool uq = false) {
+    return t.pair ? tiled_pair_fn(t.m_v, W, uq) : tiled_fn(t.m_v, t.bt, t.R, W, uq);
 }
 int k2_tiled_users(int m, int b) { return k2_tiled_shape(m, b).R; }
 bool k2_tiled_supported(int m, int b) { return k2_tiled_users(m, b) > 0; }
@@ -1078,6 +1121,7 @@ void plan_k2_tiled(const pq_index_s* idx, int B, int K, K2Plan& p) {
     // selections cost 1.4% and save 10% of a small traffic)
     static const char* qe = getenv("PQTOPK_K2_UNION");   // A/B: 0 = off
     p.qk = (sh.m_v / sh.ps) == 1 && K >= 256 && p.chunks >= 3 && p.chunks <= 64 && !(qe && *qe == '0');
+    if (p.qk) ensure_max_smem(reinterpret_cast<const void*>(tiled_fn_shape(sh, p.W, true)), (int)p.smem);
     p.st_bytes = align_up(st_table_bytes(sh, p.n_groups), 256) + (size_t)p.n_groups * R * 8 +
                  (size_t)qk_words(p) * 8 + (size_t)p.n_groups * R * p.chunks * 4;
 }
@@ -1148,7 +1192,7 @@ void launch_k2_tiled(const pq_index_s* idx, const K2Plan& p, int B, int K,
         PQ_CUDA(cudaMalloc(&a.trace, tn * 8));
         PQ_CUDA(cudaMemsetAsync(a.trace, 0, tn * 8, st));
     }
-    K2TFn fn = tiled_fn_shape(k2_tiled_shape(idx->m, idx->b), p.W);
+    K2TFn fn = tiled_fn_shape(k2_tiled_shape(idx->m, idx->b), p.W, p.qk != 0);
     launch_pdl(fn, dim3(p.grid), dim3(p.W * 32), p.smem, st, a);   // after k2_tile_S (PDL)
     count_launch();
     check_launch("k2_tiled");

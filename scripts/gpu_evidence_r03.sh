@@ -28,13 +28,15 @@ timeout 1200 ncu --set full --clock-control none --import-source on -k regex:k2_
     python bench.py --config c4 --steps 1 --warmup 3 --no-cpu-baseline --graph off --compare off > /dev/null 2>&1; echo ncu_c4=$?
 timeout 1200 ncu --set full --clock-control none --import-source on -k regex:k2_tiled -s 3 -c 1 -o gpurun_out/k2_c2_${TAG} \
     python bench.py --config c2 --steps 1 --warmup 3 --no-cpu-baseline --graph off --compare off > /dev/null 2>&1; echo ncu_c2=$?
+timeout 1500 ncu --set full --clock-control none --import-source on -k regex:k2_tiled -s 3 -c 1 -o gpurun_out/k2_c5_${TAG} \
+    python bench.py --config c5 --steps 1 --warmup 3 --no-cpu-baseline --graph off --compare off > /dev/null 2>&1; echo ncu_c5=$?
 timeout 1200 ncu --set full --clock-control none --import-source on -k regex:k6_query -s 3 -c 1 -o gpurun_out/k6_c7_${TAG} \
     python scripts/trace_k6_run.py c7 /dev/null > /dev/null 2>&1; echo ncu_c7=$?
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k7_resident -s 3 -c 1 -o gpurun_out/k7_c2a_${TAG} \
     python scripts/trace_k6_run.py c2a /dev/null > /dev/null 2>&1; echo ncu_c2a=$?
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k7_resident -s 3 -c 1 -o gpurun_out/k7_c1_${TAG} \
     python scripts/trace_k6_run.py c1 /dev/null > /dev/null 2>&1; echo ncu_c1=$?
-for r in k2_c4 k2_c2 k6_c7 k7_c2a k7_c1; do
+for r in k2_c4 k2_c2 k2_c5 k6_c7 k7_c2a k7_c1; do
   python scripts/ncu_summary.py gpurun_out/${r}_${TAG}.ncu-rep > gpurun_out/${r}_${TAG}_ncu.txt 2>&1
 done
 for c in c4 c2 c2a c1; do python scripts/launch_list.py gpurun_out/launches_${c}_${TAG}.csv > gpurun_out/launches_${c}_${TAG}_summary.txt 2>&1; done

@@ -6,7 +6,7 @@ for F in "${SETS[@]}"; do
   PQTOPK_NVCC_EXTRA="$F" python -m paper_2408_09992_b200.build --force > gpurun_out/build_k2f$i.log 2>&1; echo "build [$F] rc=$?"
   if [ -n "$TESTSEL" ]; then timeout 900 python -m pytest tests -m gpu -q -x --timeout 600 -k "$TESTSEL" > gpurun_out/gputests_k2f$i.log 2>&1; echo "[$F] tests rc=$? $(tail -1 gpurun_out/gputests_k2f$i.log)"; fi
   for c in ${CONFIGS:-c5 c4 c3}; do
-    timeout 900 python bench.py --config $c --steps ${STEPS:-5} --warmup 3 --no-cpu-baseline > gpurun_out/bench_${c}_k2f$i.log 2>&1
+    st=${STEPS:-5}; [ $c = c2 ] && st=50; timeout 900 python bench.py --config $c --steps $st --warmup 3 --no-cpu-baseline --compare off > gpurun_out/bench_${c}_k2f$i.log 2>&1
     echo "[$F] $c $(summ gpurun_out/bench_${c}_k2f$i.log)"
   done
   i=$((i+1))
