@@ -102,6 +102,13 @@ struct K2TArgs {
     int trace_stride;          // trace every trace_stride-th tile (PQTOPK_K2_TRACE_STRIDE)
     int trace_from;            // first traced tile of CTA 0 (PQTOPK_K2_TRACE_FROM)
     int* dbg;                  // diagnostics (PQTOPK_K2_DEBUG): bounded spins record state here
+    int seed_slots;            // slots per warp of the unit's first tile the seeding pass scores (<= SL, even)
+    int first_shrink;          // 1: exact K-th after every unit's first tile
+    // Balanced partition (single-phase tables): CTA x scores positions [cut[x], cut[x + 1])
+    // of the group-major (group, tile) sequence g * n_tiles + t -- one unit per group it
+    // touches; n_cut = 0: legacy units (chunk x group, round-robin)
+    int n_cut;
+    int32_t cut[K2_MAX_CUT + 1];
 };
 // Phase traces are compiled in only for diagnostics builds (PQTOPK_NVCC_EXTRA=-DK2_TRACE);
 // otherwise every trace branch folds away.
@@ -468,8 +475,7 @@ __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
         return min(a.n_tiles, t0 + a.chunk_tiles) - t0;
     };
     // TMA bulk copy: tables of (unit, phase) -> ring buffer `buf`
-    auto issue_load = [&](int64_t u, int ph, int buf) {
-        const int grp = (int)((uint32_t)u % (uint32_t)a.n_groups);
+    auto issue_load_g = [&](int grp, int ph, int buf) {
         const char* src = reinterpret_cast<const char*>(a.St) +
                           (int64_t)grp * (BT0 + (M - 1) * BT) * RB + (int64_t)ph * PS * SPLITB;
         const uint32_t bar = bar0 + 8u * buf;
@@ -480,6 +486,13 @@ __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
         for (uint32_t off = 0; off < TBLB; off += PIECE)
             bulk_g2s(tbl0 + buf * TBLB + off, src + off, PIECE < TBLB - off ? PIECE : TBLB - off, bar);
     };
+    auto issue_load = [&](int64_t u, int ph, int buf) {
+        issue_load_g((int)((uint32_t)u % (uint32_t)a.n_groups), ph, buf);
+    };
+    // balanced partition: this CTA's range of the (group, tile) sequence
+    const bool bal = NP == 1 && a.n_cut > 0;
+    int64_t blin = bal ? a.cut[blockIdx.x] : 0;
+    const int64_t bend = bal ? a.cut[blockIdx.x + 1] : 0;
     // ring sequence (phases 1 .. NP-1 of every tile, unit by unit) advanced by one
     auto advance = [&](int64_t& u, int64_t& t, int& ph) {
         if (++ph == NP) {
@@ -515,9 +528,10 @@ __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
     pdl_wait();
     pdl_trigger();                                     // K3 may be scheduled (it waits for this grid)
     // first loads: the unit's phase-0 table and ring positions 0, 1
-    if (threadIdx.x == 0 && (int64_t)blockIdx.x < units) {
+    if (threadIdx.x == 0 && (bal ? blin < bend : (int64_t)blockIdx.x < units)) {
         if constexpr (NP == 1) {
-            issue_load(blockIdx.x, 0, 0);
+            if (bal) issue_load_g((int)((uint32_t)blin / (uint32_t)a.n_tiles), 0, 0);
+            else issue_load(blockIdx.x, 0, 0);
         } else {
             issue_load(blockIdx.x, 0, RES);
             int64_t u = blockIdx.x, t = 0;
@@ -559,13 +573,34 @@ __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
     if (kTrace && a.trace && threadIdx.x == 0) {
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start_ns));
     }
-    for (int64_t unit = blockIdx.x; unit < units; unit += gridDim.x) {
+    for (int64_t unit = blockIdx.x; bal ? blin < bend : unit < units; unit += gridDim.x) {
         if (kTrace && a.trace && blockIdx.x == 0 && threadIdx.x == 0 && useq < TRACE_PH / 2)
             a.trace[(int64_t)W * TRACE_PH * 3 + 2 * useq] = clock64();
-        const int chunk = (int)((uint32_t)unit / (uint32_t)a.n_groups);
-        const int grp = (int)(unit - (int64_t)chunk * a.n_groups);
-        const int64_t tile0 = (int64_t)chunk * a.chunk_tiles;
-        const int64_t ntl = unit_tiles(unit);
+#define K2_STAMP(i) do { if (kTrace && a.dbg && blockIdx.x == 0 && threadIdx.x == 0 && useq == 0) \
+        a.dbg[32 + (i)] = (int)(clock64() - t_kstart); } while (0)
+        K2_STAMP(0);
+        int chunk, grp, next_grp;
+        int64_t tile0, ntl;
+        bool has_next;
+        if (bal) {
+            grp = (int)((uint32_t)blin / (uint32_t)a.n_tiles);
+            const int64_t g0 = (int64_t)grp * a.n_tiles;
+            tile0 = blin - g0;
+            ntl = min(bend - blin, a.n_tiles - tile0);
+            int p0 = blockIdx.x;                       // the CTA whose range holds the group's first tile
+            while (p0 > 0 && a.cut[p0] > g0) --p0;
+            chunk = (int)blockIdx.x - p0;
+            has_next = blin + ntl < bend;
+            next_grp = grp + 1;
+            blin += ntl;
+        } else {
+            chunk = (int)((uint32_t)unit / (uint32_t)a.n_groups);
+            grp = (int)(unit - (int64_t)chunk * a.n_groups);
+            tile0 = (int64_t)chunk * a.chunk_tiles;
+            ntl = unit_tiles(unit);
+            has_next = unit + gridDim.x < units;
+            next_grp = (int)((uint32_t)(unit + gridDim.x) % (uint32_t)a.n_groups);
+        }
         unsigned long long* gtau_g = a.gtau + (int64_t)grp * R;  // this group's users
         const int n_valid = min(R, a.B - grp * R);
         if (threadIdx.x < n_valid)                                // K keys >= gtau exist elsewhere
@@ -586,6 +621,7 @@ __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
         // proves a score floor, so the real first pass inserts ~K candidates
         // per user instead of the whole tile (which would then need a costly
         // shrink).
+        K2_STAMP(1);
         if constexpr (NP == 1) {
             bool any_unset = false;
             for (int u = 0; u < n_valid; ++u) any_unset |= tau_sh[u] == 0ull;
@@ -599,7 +635,7 @@ __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
                 float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
                 bool got = false;
 #pragma unroll 1
-                for (int s2 = 0; s2 < SL / 4; s2 += 2) {       // a quarter of the tile suffices
+                for (int s2 = 0; s2 < a.seed_slots; s2 += 2) {  // part of the tile suffices
                     CodePair<PSS> cpair;
                     CodePair<PSS>::check(cp + (int64_t)(s2 / 2) * 2 * RPS * CB,
                                          reinterpret_cast<const char*>(a.codes), a.codes_bytes);
@@ -642,6 +678,7 @@ __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
             }
         }
 
+        K2_STAMP(2);
         for (int64_t t = 0; t < ntl; ++t) {
             const int64_t tile = tile0 + t;
 #pragma unroll
@@ -768,7 +805,12 @@ __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
                                 if (!(cmask >> (4 * d + j) & 1u) || !(vv[j] >= tf[j])) continue;
                                 const int u = 4 * q + j;
                                 const int p = atomicAdd(&cnt_u[u], 1);
-                                if (kTrace && a.dbg) atomicAdd(reinterpret_cast<unsigned long long*>(a.dbg + 16), 1ull);   // inserts
+#ifdef K2_TRACE_INSERTS                                         // (global atomics: distorts the timeline)
+                                if (kTrace && a.dbg) {
+                                    atomicAdd(reinterpret_cast<unsigned long long*>(a.dbg + 16), 1ull);   // inserts
+                                    if (t == 0) atomicAdd(reinterpret_cast<unsigned long long*>(a.dbg + 28), 1ull);
+                                }
+#endif
                                 if (p >= a.cap) __trap();      // protocol invariant: cap >= wm + (2S + 1) TR
                                 ubuf[(int64_t)u * a.cap + p] = make_raw(vv[j] + 0.0f, row);
                                 if (p == wm) {
@@ -811,6 +853,7 @@ __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
             // barrier is sflag, fenced by its writer, and __syncwarp orders the
             // writer lane before lane 0's tiles_done store)
             const long long t_eot = kTrace ? clock64() : 0;   // diagnostics builds only
+            if (t == 0) K2_STAMP(3);
             __syncwarp();
             if (lane == 0) *reinterpret_cast<volatile int*>(&tiles_done[warp]) = (int)(tseq + 1);
             // wait until every warp has finished tile T - S (bounds the skew to S tiles)
@@ -833,7 +876,7 @@ __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
             // (always after a unit's first tile: it ran with the unit's initial,
             // usually weak or only seeded, thresholds -- an early exact K-th keeps
             // the next tiles' candidate lists short; measured: C3 -1.1%)
-            const bool need = (t == 0) || (tseq >= K2_SLACK &&
+            const bool need = (t == 0 && a.first_shrink) || (tseq >= K2_SLACK &&
                 *reinterpret_cast<volatile int*>(&sflag[(uint32_t)(tseq - K2_SLACK) % (uint32_t)(K2_SLACK + 1)]) ==
                     (int)tseq);
             const long long t_shr = kTrace ? clock64() : 0;
@@ -869,14 +912,16 @@ __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
                 atomicAdd(reinterpret_cast<unsigned long long*>(a.dbg + 20), (unsigned long long)(t_end - t_eot));
                 atomicAdd(reinterpret_cast<unsigned long long*>(a.dbg + 22), (unsigned long long)(t_end - t_shr));
             }
+            if (t == 0) K2_STAMP(4);
             ++tseq;
         }
+        K2_STAMP(5);
 
         // ---- end of unit: each user's buffer -> the unit's top-K list -------
         __syncthreads();
         if constexpr (NP == 1) {
             // every warp is done with the table: prefetch the next unit's
-            if (threadIdx.x == 0 && unit + gridDim.x < units) issue_load(unit + gridDim.x, 0, 0);
+            if (threadIdx.x == 0 && has_next) issue_load_g(next_grp, 0, 0);
         }
         for (int u = warp; u < n_valid; u += W) {
             const int gu = grp * R + u;
@@ -896,6 +941,7 @@ __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
                 union_publish(a.qk + ((int64_t)gu * a.chunks + chunk) * K2_NQ, out, nn, a.K, hist);
         }
         __syncthreads();
+        K2_STAMP(6);
         if (threadIdx.x < R) { tau_sh[threadIdx.x] = 0ull; cnt_u[threadIdx.x] = 0; nconv_u[threadIdx.x] = 0; }
         if (kTrace && a.trace && blockIdx.x == 0 && threadIdx.x == 0 && useq < TRACE_PH / 2)
             a.trace[(int64_t)W * TRACE_PH * 3 + 2 * useq + 1] = clock64();
@@ -1076,6 +1122,46 @@ static int choose_chunks_tiles(int64_t n_tiles, int n_groups, int grid_full, dou
     return best;
 }
 
+// Balanced partition for single-phase tables.  The (group, tile) pairs in group-major
+// order are cut into at most P contiguous ranges, one per CTA; a range costs its tiles
+// plus `ovh4` quarter-tiles for every group it touches (table load, seeding, first-tile
+// shrink, end-of-unit list: a unit each).  The smallest feasible bound on a range's
+// cost is found by bisection over a greedy fill.  Returns that bound (quarter-tiles)
+// and fills cut[0 .. n_cut]; 0 if no partition into <= P ranges exists.
+static int64_t balanced_cuts(int64_t T, int G, int P, int64_t ovh4, std::vector<int64_t>& cut) {
+    const int64_t total = (int64_t)G * T;
+    auto fill = [&](int64_t M4, std::vector<int64_t>* out) -> int {
+        int64_t lin = 0;
+        int np = 0;
+        if (out) { out->clear(); out->push_back(0); }
+        while (lin < total) {
+            int64_t budget = M4;
+            const int64_t lin0 = lin;
+            while (lin < total) {
+                const int64_t left = (lin / T + 1) * T - lin;
+                const int64_t avail = (budget - ovh4) / 4;
+                if (avail < 1) break;
+                const int64_t take = std::min(left, avail);
+                lin += take;
+                budget -= ovh4 + 4 * take;
+                if (take < left) break;
+            }
+            if (lin == lin0) return INT_MAX;            // not even one tile fits
+            if (out) out->push_back(lin);
+            if (++np > P) return np;
+        }
+        return np;
+    };
+    int64_t lo = ovh4 + 4, hi = 4 * total + (int64_t)G * ovh4 + 4;
+    if (fill(hi, nullptr) > P) return 0;
+    while (lo < hi) {
+        const int64_t mid = lo + (hi - lo) / 2;
+        if (fill(mid, nullptr) <= P) hi = mid; else lo = mid + 1;
+    }
+    fill(lo, &cut);
+    return lo;
+}
+
 void plan_k2_tiled(const pq_index_s* idx, int B, int K, K2Plan& p) {
     p.variant = 3;
     const pq_tuning& t = idx->tuning;
@@ -1112,6 +1198,42 @@ void plan_k2_tiled(const pq_index_s* idx, int B, int K, K2Plan& p) {
     const int64_t units = (int64_t)p.n_groups * p.chunks;
     if (units >= ((int64_t)1 << 31)) fail(PQ_ERR_UNSUPPORTED, "tiled scoring kernel: too many work units");
     p.grid = (int)std::min<int64_t>(units, t.ctas > 0 ? t.ctas : grid_full);
+    p.n_cut = 0;
+    {
+        // balanced partition (single-phase tables, no forced chunk count): taken when its
+        // modelled makespan beats the legacy units' (A/B: PQTOPK_K2_BAL=0 turns it off;
+        // PQTOPK_K2_UNIT_OVH = a unit's fixed cost in quarter-tiles)
+        static const char* be = getenv("PQTOPK_K2_BAL");
+        static const char* oe = getenv("PQTOPK_K2_UNIT_OVH");
+        const int P = t.ctas > 0 ? t.ctas : grid_full;
+        const int64_t ovh4 = oe ? std::max(0, atoi(oe)) : 8 + K / 12;
+        // Only for short jobs (< 128 tiles per CTA), where one more tile on the longest CTA
+        // and the units' fixed costs are several percent (C2: 18 -> 17 tiles, K2 208.5 ->
+        // 199.4 us).  Long jobs keep the chunk-major legacy order, in which the CTAs of all
+        // groups stream the same chunk of the codes together (one DRAM read, L2 hits for the
+        // rest) and late units start from thresholds proved by earlier ones: measured on the
+        // same box, C3 2.607 -> 2.608 ms and C5 316.2 -> 328.1 ms with this partition.
+        const bool short_job = (int64_t)p.n_groups * n_tiles < 128 * (int64_t)P || (be && *be == '2');
+        if ((sh.m_v / sh.ps) == 1 && t.chunks <= 0 && !(be && *be == '0') && P <= K2_MAX_CUT && short_job &&
+            (int64_t)p.n_groups * n_tiles < ((int64_t)1 << 31) && (int64_t)p.n_groups * n_tiles >= 2 * (int64_t)P) {
+            std::vector<int64_t> cut;
+            const int64_t m4 = balanced_cuts(n_tiles, p.n_groups, P, ovh4, cut);
+            const int64_t legacy4 = ceil_div(units, (int64_t)p.grid) * (4 * ct + ovh4);
+            if (m4 > 0 && m4 < legacy4) {
+                p.n_cut = (int)cut.size() - 1;
+                for (int i = 0; i <= p.n_cut; ++i) p.cut[i] = (int32_t)cut[i];
+                int cmax = 1;                          // lists per user = CTAs touching its group
+                for (int g = 0, lo = 0; g < p.n_groups; ++g) {
+                    while (lo + 1 < p.n_cut && cut[lo + 1] <= (int64_t)g * n_tiles) ++lo;
+                    int hi = lo;
+                    while (hi + 1 < p.n_cut && cut[hi + 1] < (int64_t)(g + 1) * n_tiles) ++hi;
+                    cmax = std::max(cmax, hi - lo + 1);
+                }
+                p.chunks = cmax;
+                p.grid = p.n_cut;
+            }
+        }
+    }
     p.lanebuf_bytes = (size_t)p.grid * R * p.cap * 8;
     p.cand_bytes = (size_t)B * p.chunks * K * 8;
     p.mscr_bytes = 0;
@@ -1146,7 +1268,10 @@ void launch_k2_tiled_prep(const pq_index_s* idx, const K2Plan& p, const float* S
     const int threads = 256;
     const int blocks = (int)std::min<int64_t>(ceil_div(total, threads), (int64_t)idx->num_sms * 16);
     unsigned long long* gtau = gtau_of(idx, p, St);
-    const int64_t nz = (int64_t)p.n_groups * p.G + qk_words(p);
+    // zeroed per call: thresholds, union floors and -- balanced partition: a group may be
+    // touched by fewer CTAs than `chunks` -- the list counts
+    const int64_t nz = (int64_t)p.n_groups * p.G + qk_words(p) +
+                       (p.n_cut > 0 ? ceil_div((int64_t)p.n_groups * p.G * p.chunks, (int64_t)2) : 0);
     if (sh.pair) launch_pdl(k2_tile_S_pair, dim3(blocks), dim3(threads), 0, st, S, B, idx->m, p.G, p.n_groups, St, gtau, nz);
     else launch_pdl(k2_tile_S, dim3(blocks), dim3(threads), 0, st, S, (const uint8_t*)idx->d_cmap3, B, idx->m, idx->b, p.G,
                     p.n_groups, St, gtau, nz);
@@ -1173,6 +1298,16 @@ void launch_k2_tiled(const pq_index_s* idx, const K2Plan& p, int B, int K,
         const int tw = idx->tuning.shrink_watermark;
         a.wm = tw > 0 ? std::min(std::max(tw, K + 1), wmax) : wmax;
     }
+    {
+        // seeding pass: a quarter of the first tile by default (A/B: PQTOPK_K2_SEEDDIV = 1, 2, 4, 8)
+        static const int sdiv = getenv("PQTOPK_K2_SEEDDIV") ? atoi(getenv("PQTOPK_K2_SEEDDIV")) : 4;
+        static const int fsh = getenv("PQTOPK_K2_FIRST_SHRINK") ? atoi(getenv("PQTOPK_K2_FIRST_SHRINK")) : 1;
+        const int SLh = 512 / p.W;                     // slots per warp per tile (SL)
+        a.seed_slots = std::max(2, (SLh / std::max(1, sdiv)) & ~1);
+        a.first_shrink = fsh;
+    }
+    a.n_cut = p.n_cut;
+    for (int i = 0; i <= p.n_cut; ++i) a.cut[i] = p.cut[i];
     a.gtau = gtau_of(idx, p, St);
     a.qk = qk_of(idx, p, St);
     a.lcnt = const_cast<int32_t*>(k2_tiled_list_counts(idx, p, St));
@@ -1197,7 +1332,7 @@ void launch_k2_tiled(const pq_index_s* idx, const K2Plan& p, int B, int K,
     count_launch();
     check_launch("k2_tiled");
     if (a.dbg) {
-        int h[28];
+        int h[64];
         PQ_CUDA(cudaMemcpyAsync(h, a.dbg, sizeof h, cudaMemcpyDeviceToHost, st));
         PQ_CUDA(cudaStreamSynchronize(st));
         cudaFree(a.dbg);
@@ -1214,6 +1349,11 @@ void launch_k2_tiled(const pq_index_s* idx, const K2Plan& p, int B, int K,
                 "inserts=%llu (%.1f per user) shrinks=%d units=%lld\n",
                 h[0], h[1], h[2], h[3], h[4], h[5], h[6], h[7], h[8], h[9], ins, (double)ins / B, h[18],
                 (long long)p.n_groups * p.chunks);
+        unsigned long long ins0 = 0;
+        memcpy(&ins0, h + 28, 8);
+        fprintf(stderr, "k2_tiled debug: first-tile inserts %llu (%.1f per user per unit); CTA 0 unit 0 cycles: start %d "
+                "seed %d..%d tile0 scored %d tile0 done %d last tile %d merged %d\n", ins0,
+                (double)ins0 / ((double)p.n_groups * p.G * p.chunks), h[32], h[33], h[34], h[35], h[36], h[37], h[38]);
     }
     if (a.trace) {                       // diagnostics only: dump CTA 0's phase timeline
         std::vector<long long> h(tn);

@@ -166,6 +166,7 @@ void launch_subscores(const float* phi, const float* psi, int B, int d, int m, i
                       float* S, cudaStream_t st);
 
 // K2 (k2_score_select.cu)
+constexpr int K2_MAX_CUT = 160;   // balanced partition: at most this many CTAs
 struct K2Plan {
     int G = 0, Ug = 0, W = 0, J = 0, cap = 0;
     int n_groups = 0, chunks = 0, grid = 0;
@@ -178,6 +179,10 @@ struct K2Plan {
     int tm = 0;
     size_t st_bytes = 0;          // v3: tiled S tables [n_groups][m][b][16] fp32 + thresholds, union floors, list counts
     bool qk = false;              // v3: union floors (large K, single-phase tables)
+    // v3 balanced partition (single-phase tables): CTA x scores the (group, tile) pairs
+    // [cut[x], cut[x + 1]) of the group-major sequence g * n_tiles + t; 0 = legacy units
+    int n_cut = 0;
+    int32_t cut[K2_MAX_CUT + 1] = {};
 };
 // K6 (k6_query.cu): the fused single-launch query kernel for B <= 4
 struct K6Plan {

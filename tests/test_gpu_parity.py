@@ -386,6 +386,42 @@ def test_tiled_parity(pq, torch, orc, case):
         assert_same(i.cpu().numpy(), s.cpu().numpy(), *ref, str(tun))
 
 
+BALANCED_CASES = [
+    # seed, N, m, b, B, K, dist, ctas -- single-phase tables; CTA ranges of the (group, tile)
+    # sequence that start mid-group, hold whole groups and end mid-group
+    (320, 50_001, 8, 256, 100, 10, "uniform", 5),     # 7 groups x 13 tiles over 5 CTAs
+    (321, 50_001, 8, 256, 100, 100, "zipf", 13),
+    (322, 150_001, 4, 16, 200, 1000, "uniform", 6),   # C5-shaped ties, R = 32, union floors off (few lists)
+    (323, 150_001, 4, 16, 130, 300, "few", 40),
+    (324, 600_001, 8, 256, 40, 10, "uniform", 0),     # default grid: 3 groups x 147 tiles over 148 CTAs
+]
+
+
+@pytest.mark.parametrize("case", BALANCED_CASES, ids=[str(c[0]) for c in BALANCED_CASES])
+def test_tiled_balanced_partition(pq, torch, orc, case):
+    """K2 v3 balanced partition (single-phase tables): each CTA scores one
+    contiguous range of the group-major (group, tile) sequence, a unit per
+    group it touches; a user's lists = the CTAs touching its group.  Bit-exact
+    against the oracle, and identical to the legacy chunk x group units."""
+    seed, N, m, b, B, K, dist, ctas = case
+    G, P, F = pqsynth.random_instance(seed, N, m, b, 4 * m, B, code_dist=dist)
+    idx = pq.pq_create(G, b=b, id_base=seed)
+    S_t = pq.pq_subscores(cuda(torch, F), cuda(torch, P))
+    ref = orc.pq_topk(G, S_t.cpu().numpy(), K, id_base=seed)
+    idx.set_tuning(variant=3, ctas=ctas)
+    plan = idx.plan(B, K)
+    R = plan["users_per_row"]
+    n_groups = -(-B // R)
+    assert plan["variant"] == 3
+    # fewer lists per user than any legacy plan filling the grid could give
+    assert plan["chunks"] <= -(-plan["ctas"] // n_groups) + 1, plan
+    i, s = pq.pq_score_topk(idx, S_t, K)
+    assert_same(i.cpu().numpy(), s.cpu().numpy(), *ref, str(plan))
+    idx.set_tuning(variant=3, ctas=ctas, shrink_watermark=1)
+    i, s = pq.pq_score_topk(idx, S_t, K)
+    assert_same(i.cpu().numpy(), s.cpu().numpy(), *ref, "shrink_watermark=1")
+
+
 @pytest.mark.parametrize("dist,chunks", [("uniform", 37), ("few", 11)])
 def test_union_floors_many_chunks(pq, torch, orc, dist, chunks):
     """Union floors (K >= 256, single-phase tables, 3..64 chunks): a unit starts
