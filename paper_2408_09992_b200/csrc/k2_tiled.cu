@@ -102,8 +102,6 @@ struct K2TArgs {
     int trace_stride;          // trace every trace_stride-th tile (PQTOPK_K2_TRACE_STRIDE)
     int trace_from;            // first traced tile of CTA 0 (PQTOPK_K2_TRACE_FROM)
     int* dbg;                  // diagnostics (PQTOPK_K2_DEBUG): bounded spins record state here
-    int seed_slots;            // slots per warp of the unit's first tile the seeding pass scores (<= SL, even)
-    int first_shrink;          // 1: exact K-th after every unit's first tile
     // Balanced partition (single-phase tables): CTA x scores positions [cut[x], cut[x + 1])
     // of the group-major (group, tile) sequence g * n_tiles + t -- one unit per group it
     // touches; n_cut = 0: legacy units (chunk x group, round-robin)
@@ -422,7 +420,9 @@ __device__ __noinline__ void union_publish(volatile unsigned long long* qo, cons
 // BT: the exact first-pair table, single-phase only — see below).
 // UQ: union floors (K2_NQ) compiled in -- a separate instantiation, selected by the
 // planner for large K, so the other configurations' kernels do not carry its code.
-template <int M, int PS, int BT, int R, int W, int D, int BT0 = BT, bool UQ = false>
+// BAL: the balanced partition (K2TArgs::cut) instead of chunk x group units -- also
+// its own instantiation (compiled into the common kernel it cost C5 2.5%).
+template <int M, int PS, int BT, int R, int W, int D, int BT0 = BT, bool UQ = false, bool BAL = false>
 __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
     constexpr int NP = M / PS;
     // table buffers: NP == 1: one; NP > 1: a 2-slot ring (buffers 0, 1) for phases
@@ -490,7 +490,7 @@ __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
         issue_load_g((int)((uint32_t)u % (uint32_t)a.n_groups), ph, buf);
     };
     // balanced partition: this CTA's range of the (group, tile) sequence
-    const bool bal = NP == 1 && a.n_cut > 0;
+    constexpr bool bal = BAL && NP == 1;
     int64_t blin = bal ? a.cut[blockIdx.x] : 0;
     const int64_t bend = bal ? a.cut[blockIdx.x + 1] : 0;
     // ring sequence (phases 1 .. NP-1 of every tile, unit by unit) advanced by one
@@ -579,10 +579,9 @@ __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
 #define K2_STAMP(i) do { if (kTrace && a.dbg && blockIdx.x == 0 && threadIdx.x == 0 && useq == 0) \
         a.dbg[32 + (i)] = (int)(clock64() - t_kstart); } while (0)
         K2_STAMP(0);
-        int chunk, grp, next_grp;
+        int chunk, grp;
         int64_t tile0, ntl;
-        bool has_next;
-        if (bal) {
+        if constexpr (bal) {
             grp = (int)((uint32_t)blin / (uint32_t)a.n_tiles);
             const int64_t g0 = (int64_t)grp * a.n_tiles;
             tile0 = blin - g0;
@@ -590,16 +589,12 @@ __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
             int p0 = blockIdx.x;                       // the CTA whose range holds the group's first tile
             while (p0 > 0 && a.cut[p0] > g0) --p0;
             chunk = (int)blockIdx.x - p0;
-            has_next = blin + ntl < bend;
-            next_grp = grp + 1;
-            blin += ntl;
+            blin += ntl;                               // (now the next unit's first position)
         } else {
             chunk = (int)((uint32_t)unit / (uint32_t)a.n_groups);
             grp = (int)(unit - (int64_t)chunk * a.n_groups);
             tile0 = (int64_t)chunk * a.chunk_tiles;
             ntl = unit_tiles(unit);
-            has_next = unit + gridDim.x < units;
-            next_grp = (int)((uint32_t)(unit + gridDim.x) % (uint32_t)a.n_groups);
         }
         unsigned long long* gtau_g = a.gtau + (int64_t)grp * R;  // this group's users
         const int n_valid = min(R, a.B - grp * R);
@@ -626,7 +621,6 @@ __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
             bool any_unset = false;
             for (int u = 0; u < n_valid; ++u) any_unset |= tau_sh[u] == 0ull;
             if (any_unset && a.K <= LM) {
-                mbar_wait(bar0, (uint32_t)(useq & 1));
                 const char* tb = reinterpret_cast<const char*>(sm_raw);
                 const int64_t tile = tile0;
                 const char* cp = reinterpret_cast<const char*>(a.codes) +
@@ -634,22 +628,36 @@ __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
                 const uint32_t row0 = (uint32_t)(tile * TR) + (uint32_t)(warp * SL * RPS) + (uint32_t)(lane / LPR);
                 float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
                 bool got = false;
-#pragma unroll 1
-                for (int s2 = 0; s2 < a.seed_slots; s2 += 2) {  // part of the tile suffices
-                    CodePair<PSS> cpair;
-                    CodePair<PSS>::check(cp + (int64_t)(s2 / 2) * 2 * RPS * CB,
+                // a quarter of the tile suffices; every code word and padding flag is
+                // requested before the wait for the table, so the pass itself is SEEDP
+                // slot pairs of shared-memory gathers (it was a chain of dependent global
+                // loads; C2 K2 -1% on the same box)
+                constexpr int SEEDP = SL / 8;
+                CodePair<PSS> cps[SEEDP];
+                int32_t pad[SEEDP][2];
+#pragma unroll
+                for (int i = 0; i < SEEDP; ++i) {
+                    CodePair<PSS>::check(cp + (int64_t)i * 2 * RPS * CB,
                                          reinterpret_cast<const char*>(a.codes), a.codes_bytes);
-                    cpair.load(cp + (int64_t)(s2 / 2) * 2 * RPS * CB);
+                    cps[i].load(cp + (int64_t)i * 2 * RPS * CB);
+                }
+#pragma unroll
+                for (int i = 0; i < SEEDP; ++i)
+#pragma unroll
+                    for (int e = 0; e < 2; ++e) pad[i][e] = __ldg(&a.perm[row0 + (uint32_t)(2 * i + e) * RPS]);
+                mbar_wait(bar0, (uint32_t)(useq & 1));
+#pragma unroll
+                for (int i = 0; i < SEEDP; ++i) {
 #pragma unroll
                     for (int e = 0; e < 2; ++e) {
                         float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
                         for (int kk = 0; kk < PS; ++kk) {
-                            const uint32_t off = cpair.template off<RB>(e, kk, q16);
+                            const uint32_t off = cps[i].template off<RB>(e, kk, q16);
                             const float4 v = lds128(tb + split_off(kk) + off);
                             if (kk == 0) acc = v; else add4(acc, v);
                         }
-                        if (a.perm[row0 + (uint32_t)(s2 + e) * RPS] >= 0) {
+                        if (pad[i][e] >= 0) {
                             got = true;
                             mx[0] = fmaxf(mx[0], acc.x); mx[1] = fmaxf(mx[1], acc.y);
                             mx[2] = fmaxf(mx[2], acc.z); mx[3] = fmaxf(mx[3], acc.w);
@@ -876,7 +884,7 @@ __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
             // (always after a unit's first tile: it ran with the unit's initial,
             // usually weak or only seeded, thresholds -- an early exact K-th keeps
             // the next tiles' candidate lists short; measured: C3 -1.1%)
-            const bool need = (t == 0 && a.first_shrink) || (tseq >= K2_SLACK &&
+            const bool need = (t == 0) || (tseq >= K2_SLACK &&
                 *reinterpret_cast<volatile int*>(&sflag[(uint32_t)(tseq - K2_SLACK) % (uint32_t)(K2_SLACK + 1)]) ==
                     (int)tseq);
             const long long t_shr = kTrace ? clock64() : 0;
@@ -899,7 +907,8 @@ __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
                         }
                     }
                 }
-                // adopt thresholds proved by other CTAs on other chunks of these users
+                // adopt thresholds proved by other CTAs on other chunks of these users (loading
+                // them before the selections measured 2% slower on C2)
                 if (threadIdx.x < n_valid)
                     atomicMax(&tau_sh[threadIdx.x], *reinterpret_cast<volatile unsigned long long*>(&gtau_g[threadIdx.x]));
                 __syncthreads();
@@ -921,7 +930,13 @@ __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
         __syncthreads();
         if constexpr (NP == 1) {
             // every warp is done with the table: prefetch the next unit's
-            if (threadIdx.x == 0 && has_next) issue_load_g(next_grp, 0, 0);
+            // (nothing about the next unit is kept live across the tile loop: two more
+            // registers there cost C5 2.5%)
+            if constexpr (bal) {
+                if (threadIdx.x == 0 && blin < bend) issue_load_g(grp + 1, 0, 0);
+            } else {
+                if (threadIdx.x == 0 && unit + gridDim.x < units) issue_load(unit + gridDim.x, 0, 0);
+            }
         }
         for (int u = warp; u < n_valid; u += W) {
             const int gu = grp * R + u;
@@ -1026,9 +1041,13 @@ __global__ void k2_tile_S_pair(const float* __restrict__ S, int B, int m, int R,
 typedef void (*K2TFn)(const K2TArgs);
 
 template <int M, int PS, int BT, int R, int BT0 = BT>
-static K2TFn tiled_fn_w(int W, bool uq) {
+static K2TFn tiled_fn_w(int W, bool uq, bool bal) {
     // deeper code prefetch for m = 16 (C4: -1.7 %; m = 8 and m = 64 prefer 4)
-    if constexpr (M == PS) {                           // single-phase tables: a union-floor variant
+    if constexpr (M == PS) {                           // single-phase tables: balanced / union-floor variants
+        if (bal) {
+            if (W == 16) return k2_tiled<M, PS, BT, R, 16, 4, BT0, false, true>;
+            return k2_tiled<M, PS, BT, R, 8, 4, BT0, false, true>;
+        }
         if (uq) {
             if (W == 16) return k2_tiled<M, PS, BT, R, 16, 4, BT0, true>;
             return k2_tiled<M, PS, BT, R, 8, 4, BT0, true>;
@@ -1041,28 +1060,28 @@ static K2TFn tiled_fn_w(int W, bool uq) {
 // 256-row "split" whose row c = g0 + 16 g1 holds fl(S[0][g0] + S[1][g1]) -- the
 // first partial sum of Eq. 5 exactly as the sequential order computes it -- so
 // an item costs m - 1 lookups.
-static K2TFn tiled_pair_fn(int m_v, int W, bool uq = false) {
-    if (m_v == 3) return tiled_fn_w<3, 3, 16, 32, 256>(W, uq);
-    if (m_v == 7) return tiled_fn_w<7, 7, 16, 32, 256>(W, uq);
+static K2TFn tiled_pair_fn(int m_v, int W, bool uq = false, bool bal = false) {
+    if (m_v == 3) return tiled_fn_w<3, 3, 16, 32, 256>(W, uq, bal);
+    if (m_v == 7) return tiled_fn_w<7, 7, 16, 32, 256>(W, uq, bal);
     return nullptr;
 }
 // Instantiated shapes: R = 16 (paired layout) for b = 256, m in {8, 16, 32, 64};
 // R = 32 (item order) when the 32-user table fits: (m, b) in {(4, 16), (8, 16), (4, 256)}.
-static K2TFn tiled_fn(int m, int b, int R, int W, bool uq = false) {
+static K2TFn tiled_fn(int m, int b, int R, int W, bool uq = false, bool bal = false) {
     if (R == 16 && b == 256) {
-        if (m == 16) return tiled_fn_w<16, 4, 256, 16>(W, uq);
-        if (m == 8) return tiled_fn_w<8, 8, 256, 16>(W, uq);
+        if (m == 16) return tiled_fn_w<16, 4, 256, 16>(W, uq, bal);
+        if (m == 8) return tiled_fn_w<8, 8, 256, 16>(W, uq, bal);
     }
     if (R == 32 && b == 16) {
-        if (m == 4) return tiled_fn_w<4, 4, 16, 32>(W, uq);
-        if (m == 8) return tiled_fn_w<8, 8, 16, 32>(W, uq);
+        if (m == 4) return tiled_fn_w<4, 4, 16, 32>(W, uq, bal);
+        if (m == 8) return tiled_fn_w<8, 8, 16, 32>(W, uq, bal);
     }
-    if (R == 32 && b == 256 && m == 4) return tiled_fn_w<4, 4, 256, 32>(W, uq);
+    if (R == 32 && b == 256 && m == 4) return tiled_fn_w<4, 4, 256, 32>(W, uq, bal);
     // many splits (Fig. 2b's m = 64): 16 users, phases of 4 splits; pq_create pairs
     // items on complementary colours over the first 20 splits (64-split signatures
     // have no complements), so those splits' gathers are conflict-free
-    if (R == 16 && b == 256 && m == 32) return tiled_fn_w<32, 4, 256, 16>(W, uq);
-    if (R == 16 && b == 256 && m == 64) return tiled_fn_w<64, 4, 256, 16>(W, uq);
+    if (R == 16 && b == 256 && m == 32) return tiled_fn_w<32, 4, 256, 16>(W, uq, bal);
+    if (R == 16 && b == 256 && m == 64) return tiled_fn_w<64, 4, 256, 16>(W, uq, bal);
     return nullptr;
 }
 int k2_tiled_ps(int m) { return m >= 16 ? 4 : m; }
@@ -1081,8 +1100,8 @@ TiledShape k2_tiled_shape(int m, int b) {
     t.pss = (t.ps == 3 || t.ps == 7) ? t.ps + 1 : t.ps;
     return t;
 }
-static K2TFn tiled_fn_shape(const TiledShape& t, int W, bool uq = false) {
-    return t.pair ? tiled_pair_fn(t.m_v, W, uq) : tiled_fn(t.m_v, t.bt, t.R, W, uq);
+static K2TFn tiled_fn_shape(const TiledShape& t, int W, bool uq = false, bool bal = false) {
+    return t.pair ? tiled_pair_fn(t.m_v, W, uq, bal) : tiled_fn(t.m_v, t.bt, t.R, W, uq, bal);
 }
 int k2_tiled_users(int m, int b) { return k2_tiled_shape(m, b).R; }
 bool k2_tiled_supported(int m, int b) { return k2_tiled_users(m, b) > 0; }
@@ -1242,8 +1261,10 @@ void plan_k2_tiled(const pq_index_s* idx, int B, int K, K2Plan& p) {
     // bytes 8.2 -> 4.3 GB, time -0.5%).  Not for K = 100 (C3: the unit-end level
     // selections cost 1.4% and save 10% of a small traffic)
     static const char* qe = getenv("PQTOPK_K2_UNION");   // A/B: 0 = off
-    p.qk = (sh.m_v / sh.ps) == 1 && K >= 256 && p.chunks >= 3 && p.chunks <= 64 && !(qe && *qe == '0');
+    p.qk = (sh.m_v / sh.ps) == 1 && K >= 256 && p.chunks >= 3 && p.chunks <= 64 && p.n_cut == 0 &&
+           !(qe && *qe == '0');
     if (p.qk) ensure_max_smem(reinterpret_cast<const void*>(tiled_fn_shape(sh, p.W, true)), (int)p.smem);
+    if (p.n_cut > 0) ensure_max_smem(reinterpret_cast<const void*>(tiled_fn_shape(sh, p.W, false, true)), (int)p.smem);
     p.st_bytes = align_up(st_table_bytes(sh, p.n_groups), 256) + (size_t)p.n_groups * R * 8 +
                  (size_t)qk_words(p) * 8 + (size_t)p.n_groups * R * p.chunks * 4;
 }
@@ -1298,14 +1319,6 @@ void launch_k2_tiled(const pq_index_s* idx, const K2Plan& p, int B, int K,
         const int tw = idx->tuning.shrink_watermark;
         a.wm = tw > 0 ? std::min(std::max(tw, K + 1), wmax) : wmax;
     }
-    {
-        // seeding pass: a quarter of the first tile by default (A/B: PQTOPK_K2_SEEDDIV = 1, 2, 4, 8)
-        static const int sdiv = getenv("PQTOPK_K2_SEEDDIV") ? atoi(getenv("PQTOPK_K2_SEEDDIV")) : 4;
-        static const int fsh = getenv("PQTOPK_K2_FIRST_SHRINK") ? atoi(getenv("PQTOPK_K2_FIRST_SHRINK")) : 1;
-        const int SLh = 512 / p.W;                     // slots per warp per tile (SL)
-        a.seed_slots = std::max(2, (SLh / std::max(1, sdiv)) & ~1);
-        a.first_shrink = fsh;
-    }
     a.n_cut = p.n_cut;
     for (int i = 0; i <= p.n_cut; ++i) a.cut[i] = p.cut[i];
     a.gtau = gtau_of(idx, p, St);
@@ -1327,7 +1340,7 @@ void launch_k2_tiled(const pq_index_s* idx, const K2Plan& p, int B, int K,
         PQ_CUDA(cudaMalloc(&a.trace, tn * 8));
         PQ_CUDA(cudaMemsetAsync(a.trace, 0, tn * 8, st));
     }
-    K2TFn fn = tiled_fn_shape(k2_tiled_shape(idx->m, idx->b), p.W, p.qk != 0);
+    K2TFn fn = tiled_fn_shape(k2_tiled_shape(idx->m, idx->b), p.W, p.qk != 0, p.n_cut > 0);
     launch_pdl(fn, dim3(p.grid), dim3(p.W * 32), p.smem, st, a);   // after k2_tile_S (PDL)
     count_launch();
     check_launch("k2_tiled");

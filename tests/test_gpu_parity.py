@@ -364,6 +364,11 @@ TILED_CASES = [
     # 2^m distinct tuples, K = 4000, every tile floods the buffers at the threshold
     (311, 400_003, 8, 256, 16, 4000, "few"),
     (312, 200_003, 16, 256, 16, 4000, "few"),        # m = 16: TMEM phases
+    # small K on single-phase tables: small lists per unit, seeded thresholds, first-tile shrink (the
+    # C2 regime)
+    (314, 123_457, 8, 256, 20, 10, "zipf"),
+    (315, 90_001, 8, 16, 33, 16, "few"),             # ties
+    (316, 200_001, 4, 256, 40, 32, "uniform"),
 ]
 
 
@@ -394,6 +399,8 @@ BALANCED_CASES = [
     (322, 150_001, 4, 16, 200, 1000, "uniform", 6),   # C5-shaped ties, R = 32, union floors off (few lists)
     (323, 150_001, 4, 16, 130, 300, "few", 40),
     (324, 600_001, 8, 256, 40, 10, "uniform", 0),     # default grid: 3 groups x 147 tiles over 148 CTAs
+    (325, 300_001, 8, 256, 20, 10, "few", 20),        # heavy ties
+    (326, 300_001, 8, 256, 70, 3, "uniform", 37),
 ]
 
 
