@@ -53,6 +53,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <type_traits>
 #include <vector>
 
 #include "k2_common.cuh"
@@ -259,12 +260,54 @@ __device__ __forceinline__ uint64_t warp_kth_regs(const uint64_t (&v)[SR], int n
     return prefix;
 }
 
+// shrink_user for a buffer of at most 32 * SR entries, selected in registers: one read
+// of the buffer instead of one per radix pass.
+template <int SR>
+__device__ __forceinline__ uint64_t shrink_user_regs(uint64_t* ub, int nc, int n, int K, uint64_t floor,
+                                                     uint64_t* dst, uint32_t* hist, const int32_t* perm,
+                                                     uint32_t id_base, int& n_out) {
+    const int lane = threadIdx.x & 31;
+    uint64_t v[SR];
+#pragma unroll
+    for (int u = 0; u < SR; ++u) {
+        const int i = u * 32 + lane;
+        v[u] = i < n ? ub[i] : 0ull;
+    }
+    int32_t lid[SR];
+#pragma unroll
+    for (int u = 0; u < SR; ++u) {
+        const int i = u * 32 + lane;
+        lid[u] = (i >= nc && i < n) ? __ldg(&perm[(uint32_t)v[u]]) : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < SR; ++u) {
+        const int i = u * 32 + lane;
+        if (i >= nc && i < n)
+            v[u] = lid[u] < 0 ? 0ull
+                              : ((v[u] & 0xFFFFFFFF00000000ull) | (uint64_t)(0xFFFFFFFFu - (id_base + (uint32_t)lid[u])));
+    }
+    const uint64_t kth = n > K ? warp_kth_regs<SR>(v, n, (uint32_t)K, hist) : 0ull;
+    uint64_t th = kth > floor ? kth : floor;
+    if (th == 0ull) th = 1ull;                               // key 0 = padding: never kept
+    int pos = 0;
+#pragma unroll
+    for (int u = 0; u < SR; ++u) {
+        const bool keep = u * 32 + lane < n && v[u] >= th;
+        const unsigned bm = __ballot_sync(FULL, keep);
+        if (keep) dst[pos + __popc(bm & lanemask_lt())] = v[u];
+        pos += __popc(bm);
+    }
+    n_out = pos;
+    return kth;
+}
+
 // Whole warp, one user: convert the raw tail, then keep only keys >= the K-th
 // best (and >= `floor`), writing them to `dst` (may alias ub).  Returns the
 // K-th key (0 if the buffer has fewer than K non-zero keys) and the count.
 // Buffers of up to 256 entries (a shrink at the watermark 2K + 64 for K <= 96,
-// e.g. C2's K = 10) are selected in registers: one read of the buffer instead
-// of one per radix pass (a larger register window spills in the caller).
+// e.g. C2's K = 10) are selected in registers, 2, 4 or 8 entries per lane (C2's
+// first-tile shrink holds ~40 entries, its end-of-unit list ~140; a larger
+// register window spills in the caller).
 __device__ __noinline__ uint64_t shrink_user(uint64_t* ub, int nc, int n, int K, uint64_t floor,
                                              uint64_t* dst, uint32_t* hist, const int32_t* perm,
                                              uint32_t id_base, int& n_out) {
@@ -273,39 +316,9 @@ __device__ __noinline__ uint64_t shrink_user(uint64_t* ub, int nc, int n, int K,
         return lid < 0 ? 0ull
                        : ((raw & 0xFFFFFFFF00000000ull) | (uint64_t)(0xFFFFFFFFu - (id_base + (uint32_t)lid)));
     };
-    constexpr int SR = 8;
-    if (n <= 32 * SR) {
-        uint64_t v[SR];
-#pragma unroll
-        for (int u = 0; u < SR; ++u) {
-            const int i = u * 32 + lane;
-            v[u] = i < n ? ub[i] : 0ull;
-        }
-        int32_t lid[SR];
-#pragma unroll
-        for (int u = 0; u < SR; ++u) {
-            const int i = u * 32 + lane;
-            lid[u] = (i >= nc && i < n) ? __ldg(&perm[(uint32_t)v[u]]) : 0;
-        }
-#pragma unroll
-        for (int u = 0; u < SR; ++u) {
-            const int i = u * 32 + lane;
-            if (i >= nc && i < n) v[u] = to_key(v[u], lid[u]);
-        }
-        const uint64_t kth = n > K ? warp_kth_regs<SR>(v, n, (uint32_t)K, hist) : 0ull;
-        uint64_t th = kth > floor ? kth : floor;
-        if (th == 0ull) th = 1ull;                               // key 0 = padding: never kept
-        int pos = 0;
-#pragma unroll
-        for (int u = 0; u < SR; ++u) {
-            const bool keep = u * 32 + lane < n && v[u] >= th;
-            const unsigned bm = __ballot_sync(FULL, keep);
-            if (keep) dst[pos + __popc(bm & lanemask_lt())] = v[u];
-            pos += __popc(bm);
-        }
-        n_out = pos;
-        return kth;
-    }
+    if (n <= 64) return shrink_user_regs<2>(ub, nc, n, K, floor, dst, hist, perm, id_base, n_out);
+    if (n <= 128) return shrink_user_regs<4>(ub, nc, n, K, floor, dst, hist, perm, id_base, n_out);
+    if (n <= 256) return shrink_user_regs<8>(ub, nc, n, K, floor, dst, hist, perm, id_base, n_out);
     constexpr int U = 8;                               // independent loads in flight per lane
     for (int i0 = nc; i0 < n; i0 += 32 * U) {
         uint64_t r[U];
@@ -467,12 +480,19 @@ __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
     const uint32_t tbl0 = smem_u32(sm_raw);
     const uint32_t bar0 = smem_u32(mbar);
 
-    const int64_t units = (int64_t)a.n_groups * a.chunks;
-    // units < 2^31 (user groups x chunks): 32-bit unsigned division, no 64-bit call
-    auto unit_tiles = [&](int64_t u) -> int64_t {
-        const int64_t ch = (int64_t)((uint32_t)u / (uint32_t)a.n_groups);
-        const int64_t t0 = ch * a.chunk_tiles;
-        return min(a.n_tiles, t0 + a.chunk_tiles) - t0;
+    // Unit, tile and sequence counters are 32-bit (the planner bounds units and tiles by
+    // 2^31; the sequence counters are only compared modulo small powers of two or over
+    // short distances): 64-bit ones hold ~8 more registers live across the tile loop
+    // (same-box A/B: C4 0.8782 -> 0.880, C3 +0.2%, C2 +0.5%).  The first-pair-table
+    // kernels (C5) keep the 64-bit ones: their allocation came out 2.2% slower with 32.
+    constexpr bool WIDE = BT0 != BT;
+    using ctr_t = std::conditional_t<WIDE, int64_t, int>;
+    using uctr_t = std::conditional_t<WIDE, int64_t, uint32_t>;
+    const ctr_t n_tiles = (ctr_t)a.n_tiles, chunk_tiles = (ctr_t)a.chunk_tiles;
+    const uctr_t units = (uctr_t)a.n_groups * (uctr_t)a.chunks;
+    auto unit_tiles = [&](uctr_t u) -> ctr_t {
+        const ctr_t t0 = (ctr_t)((uint32_t)u / (uint32_t)a.n_groups) * chunk_tiles;
+        return min(n_tiles, t0 + chunk_tiles) - t0;
     };
     // TMA bulk copy: tables of (unit, phase) -> ring buffer `buf`
     auto issue_load_g = [&](int grp, int ph, int buf) {
@@ -486,15 +506,15 @@ __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
         for (uint32_t off = 0; off < TBLB; off += PIECE)
             bulk_g2s(tbl0 + buf * TBLB + off, src + off, PIECE < TBLB - off ? PIECE : TBLB - off, bar);
     };
-    auto issue_load = [&](int64_t u, int ph, int buf) {
+    auto issue_load = [&](uctr_t u, int ph, int buf) {
         issue_load_g((int)((uint32_t)u % (uint32_t)a.n_groups), ph, buf);
     };
     // balanced partition: this CTA's range of the (group, tile) sequence
     constexpr bool bal = BAL && NP == 1;
-    int64_t blin = bal ? a.cut[blockIdx.x] : 0;
-    const int64_t bend = bal ? a.cut[blockIdx.x + 1] : 0;
+    ctr_t blin = bal ? a.cut[blockIdx.x] : 0;
+    const ctr_t bend = bal ? a.cut[blockIdx.x + 1] : 0;
     // ring sequence (phases 1 .. NP-1 of every tile, unit by unit) advanced by one
-    auto advance = [&](int64_t& u, int64_t& t, int& ph) {
+    auto advance = [&](uctr_t& u, ctr_t& t, int& ph) {
         if (++ph == NP) {
             ph = 1;
             if (++t == unit_tiles(u)) { t = 0; u += gridDim.x; }
@@ -528,13 +548,14 @@ __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
     pdl_wait();
     pdl_trigger();                                     // K3 may be scheduled (it waits for this grid)
     // first loads: the unit's phase-0 table and ring positions 0, 1
-    if (threadIdx.x == 0 && (bal ? blin < bend : (int64_t)blockIdx.x < units)) {
+    if (threadIdx.x == 0 && (bal ? blin < bend : (uctr_t)blockIdx.x < units)) {
         if constexpr (NP == 1) {
-            if (bal) issue_load_g((int)((uint32_t)blin / (uint32_t)a.n_tiles), 0, 0);
+            if (bal) issue_load_g((int)((uint32_t)blin / (uint32_t)n_tiles), 0, 0);
             else issue_load(blockIdx.x, 0, 0);
         } else {
             issue_load(blockIdx.x, 0, RES);
-            int64_t u = blockIdx.x, t = 0;
+            uctr_t u = blockIdx.x;
+            ctr_t t = 0;
             int ph = 1;
             for (int i = 0; i < 2 && u < units; ++i) {
                 issue_load(u, ph, i);
@@ -551,8 +572,8 @@ __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
     const int q = lane % LPR;                          // user quad
     const uint32_t q16 = (uint32_t)q * 16u;
     uint64_t* ubuf = a.ubuf + (int64_t)blockIdx.x * R * a.cap;
-    int64_t gseq = 0;                                  // table uses so far (NP > 1)
-    int64_t useq = 0;                                  // units done by this CTA (NP == 1)
+    uctr_t gseq = 0;                                   // table uses so far (NP > 1)
+    uctr_t useq = 0;                                   // units done by this CTA (NP == 1)
     // Shrink protocol (no per-tile barrier), with a skew allowance of S = slack
     // tiles: the insert that takes a user's buffer to `wm` entries during tile
     // T records T + S in sflag[T % (S + 1)]; at the end of tile T + S every warp
@@ -565,7 +586,7 @@ __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
     // tiles up to T + S that is at most (2S + 1) * TR entries per user before
     // the shrink: cap >= wm + (2S + 1) * TR.
     const int wm = a.wm;
-    int64_t tseq = 0;                                  // tiles done by this CTA
+    ctr_t tseq = 0;                                    // tiles done by this CTA
 
     constexpr int64_t PSTR = 2 * RPS * CB;             // code bytes per slot pair
     constexpr int DP = D / 2;                          // slot pairs per group
@@ -573,27 +594,27 @@ __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
     if (kTrace && a.trace && threadIdx.x == 0) {
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start_ns));
     }
-    for (int64_t unit = blockIdx.x; bal ? blin < bend : unit < units; unit += gridDim.x) {
+    for (uctr_t unit = blockIdx.x; bal ? blin < bend : unit < units; unit += gridDim.x) {
         if (kTrace && a.trace && blockIdx.x == 0 && threadIdx.x == 0 && useq < TRACE_PH / 2)
             a.trace[(int64_t)W * TRACE_PH * 3 + 2 * useq] = clock64();
 #define K2_STAMP(i) do { if (kTrace && a.dbg && blockIdx.x == 0 && threadIdx.x == 0 && useq == 0) \
         a.dbg[32 + (i)] = (int)(clock64() - t_kstart); } while (0)
         K2_STAMP(0);
         int chunk, grp;
-        int64_t tile0, ntl;
+        ctr_t tile0, ntl;
         if constexpr (bal) {
-            grp = (int)((uint32_t)blin / (uint32_t)a.n_tiles);
-            const int64_t g0 = (int64_t)grp * a.n_tiles;
+            grp = (int)((uint32_t)blin / (uint32_t)n_tiles);
+            const ctr_t g0 = (ctr_t)grp * n_tiles;
             tile0 = blin - g0;
-            ntl = min(bend - blin, a.n_tiles - tile0);
+            ntl = min(bend - blin, n_tiles - tile0);
             int p0 = blockIdx.x;                       // the CTA whose range holds the group's first tile
             while (p0 > 0 && a.cut[p0] > g0) --p0;
             chunk = (int)blockIdx.x - p0;
             blin += ntl;                               // (now the next unit's first position)
         } else {
             chunk = (int)((uint32_t)unit / (uint32_t)a.n_groups);
-            grp = (int)(unit - (int64_t)chunk * a.n_groups);
-            tile0 = (int64_t)chunk * a.chunk_tiles;
+            grp = (int)(unit - (uctr_t)chunk * (uctr_t)a.n_groups);
+            tile0 = (ctr_t)chunk * chunk_tiles;
             ntl = unit_tiles(unit);
         }
         unsigned long long* gtau_g = a.gtau + (int64_t)grp * R;  // this group's users
@@ -687,7 +708,7 @@ __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
         }
 
         K2_STAMP(2);
-        for (int64_t t = 0; t < ntl; ++t) {
+        for (ctr_t t = 0; t < ntl; ++t) {
             const int64_t tile = tile0 + t;
 #pragma unroll
             for (int ph = 0; ph < NP; ++ph) {
@@ -844,7 +865,8 @@ __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
                             if (ph == 0) {             // resident table: reload after the unit's last tile
                                 if (t + 1 == ntl && unit + gridDim.x < units) issue_load(unit + gridDim.x, 0, RES);
                             } else {                   // ring: load the position this slot serves next
-                                int64_t u2 = unit, t2 = t;
+                                uctr_t u2 = unit;
+                                ctr_t t2 = t;
                                 int ph2 = ph;
                                 for (int st = 0; st < 2; ++st) advance(u2, t2, ph2);
                                 if (u2 < units) issue_load(u2, ph2, buf);

@@ -10,7 +10,7 @@ mkdir -p gpurun_out/checked
 TAG=${TAG:-chk}
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/checked/build.log 2>&1; echo build=$?
 python -m paper_2408_09992_b200.build --checked >> gpurun_out/checked/build.log 2>&1; echo build_checked=$?
-for c in ${CASES:-tiled16 tiled8 tiled4 latency k6grid k6clus k6pair k7 k7clus merge subset recjpq dense}; do
+for c in ${CASES:-tiled16 tiled8 tiled4 tiledbal latency k6grid k6clus k6pair k7 k7clus merge subset recjpq dense}; do
   log=gpurun_out/checked/case_${c}_${TAG}.log
   PQTOPK_CHECKED=1 timeout ${TLIM:-600} python scripts/sanitize_cases.py --reps ${REPS:-20} $c > $log 2>&1
   rc=$?

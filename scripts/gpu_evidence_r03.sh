@@ -1,4 +1,4 @@
-# Round-3 evidence: build, smoke, full GPU tests, default bench line (C4 with
+# Evidence pass (rounds 3+): build, smoke, full GPU tests, default bench line (C4 with
 # cpu_baseline), every config's bench line, one-rank NCCL path, reference arm,
 # ncu launch lists, ncu --set full of the dominant kernel per path.
 # usage: TAG=r03g bash scripts/gpu_evidence_r03.sh
@@ -39,5 +39,6 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:k7_r
 for r in k2_c4 k2_c2 k2_c5 k6_c7 k7_c2a k7_c1; do
   python scripts/ncu_summary.py gpurun_out/${r}_${TAG}.ncu-rep > gpurun_out/${r}_${TAG}_ncu.txt 2>&1
 done
+rm -f gpurun_out/*_${TAG}.ncu-rep   # (summarised above; gpurun brings back at most 64 MiB)
 for c in c4 c2 c2a c1; do python scripts/launch_list.py gpurun_out/launches_${c}_${TAG}.csv > gpurun_out/launches_${c}_${TAG}_summary.txt 2>&1; done
 echo done

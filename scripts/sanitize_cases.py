@@ -11,6 +11,8 @@ checked library).  Cases (SURVEY.md §5 "race detection"):
             (forces the tile-end shrink protocol on every tile)
   tiled8    K2 v3 m = 8 single-phase tables with threshold seeding, shrink_watermark = 1
   tiled4    K2 v3 b = 16 exact first-pair tables, K = 300 (massive ties)
+  tiledbal  K2 v3 balanced partition (CTA ranges of the (group, tile) sequence that start
+            mid-group, hold whole groups and end mid-group), shrink_watermark = 1
   latency   K2 v4 (B <= 4 through pq_score_topk) + K1 + K3
   k6grid    K6 fused query, cooperative grid mode
   k6clus    K6 fused query, cluster mode (cluster = 2)
@@ -70,6 +72,9 @@ def main(cases):
             tiled(9002, 20_011, 8, 256, 64, 32, 20, shrink_watermark=1)
         elif c == "tiled4":
             tiled(9003, 30_001, 4, 16, 16, 32, 300, dist="uniform")
+        elif c == "tiledbal":
+            tiled(9014, 50_001, 8, 256, 64, 100, 10, ctas=5, shrink_watermark=1)
+            tiled(9015, 150_001, 4, 16, 16, 130, 300, dist="few", ctas=40)
         elif c == "latency":
             G, P, F = pqsynth.random_instance(9004, 30_001, 8, 256, 64, 2)
             idx = pq.pq_create(G, b=256)
@@ -159,7 +164,7 @@ if __name__ == "__main__":
     reps = 1
     if argv[:1] == ["--reps"]:
         reps, argv = int(argv[1]), argv[2:]
-    cases = argv or ["tiled16", "tiled8", "tiled4", "latency", "k6grid", "k6clus", "k6pair", "k7", "k7clus", "merge",
+    cases = argv or ["tiled16", "tiled8", "tiled4", "tiledbal", "latency", "k6grid", "k6clus", "k6pair", "k7", "k7clus", "merge",
                      "subset", "recjpq", "dense"]
     import paper_2408_09992_b200 as _pq
     print("library:", _pq.lib_path(), flush=True)
