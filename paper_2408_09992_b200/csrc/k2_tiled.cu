@@ -308,6 +308,11 @@ __device__ __forceinline__ uint64_t shrink_user_regs(uint64_t* ub, int nc, int n
 // e.g. C2's K = 10) are selected in registers, 2, 4 or 8 entries per lane (C2's
 // first-tile shrink holds ~40 entries, its end-of-unit list ~140; a larger
 // register window spills in the caller).
+// BIG: register windows of 12 and 16 entries per lane too (K = 100 shrinks at 264+
+// entries: C3 -0.25%, C2 -0.85%).  Not for the first-pair-table kernels (C5, K = 1000:
+// buffers far beyond 512 entries), whose allocation around the call came out 2.5% slower
+// with the larger callee.
+template <bool BIG>
 __device__ __noinline__ uint64_t shrink_user(uint64_t* ub, int nc, int n, int K, uint64_t floor,
                                              uint64_t* dst, uint32_t* hist, const int32_t* perm,
                                              uint32_t id_base, int& n_out) {
@@ -319,6 +324,10 @@ __device__ __noinline__ uint64_t shrink_user(uint64_t* ub, int nc, int n, int K,
     if (n <= 64) return shrink_user_regs<2>(ub, nc, n, K, floor, dst, hist, perm, id_base, n_out);
     if (n <= 128) return shrink_user_regs<4>(ub, nc, n, K, floor, dst, hist, perm, id_base, n_out);
     if (n <= 256) return shrink_user_regs<8>(ub, nc, n, K, floor, dst, hist, perm, id_base, n_out);
+    if constexpr (BIG) {
+        if (n <= 384) return shrink_user_regs<12>(ub, nc, n, K, floor, dst, hist, perm, id_base, n_out);
+        if (n <= 512) return shrink_user_regs<16>(ub, nc, n, K, floor, dst, hist, perm, id_base, n_out);
+    }
     constexpr int U = 8;                               // independent loads in flight per lane
     for (int i0 = nc; i0 < n; i0 += 32 * U) {
         uint64_t r[U];
@@ -918,7 +927,7 @@ __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
                     if (n <= a.K) continue;
                     uint64_t* ub = ubuf + (int64_t)u * a.cap;
                     int nn;
-                    const uint64_t kth = shrink_user(ub, nconv_u[u], n, a.K, tau_sh[u], ub, hist,
+                    const uint64_t kth = shrink_user<BT0 == BT>(ub, nconv_u[u], n, a.K, tau_sh[u], ub, hist,
                                                      a.perm, a.id_base, nn);
                     if (lane == 0) {
                         cnt_u[u] = nn;
@@ -966,7 +975,7 @@ __global__ void __launch_bounds__(W * 32, 1) k2_tiled(const K2TArgs a) {
             uint64_t* out = a.cand + ((int64_t)gu * a.chunks + chunk) * a.K;
             uint64_t* ub = ubuf + (int64_t)u * a.cap;
             int nn;
-            const uint64_t kth = shrink_user(ub, nconv_u[u], cnt_u[u], a.K, tau_sh[u], out, hist,
+            const uint64_t kth = shrink_user<BT0 == BT>(ub, nconv_u[u], cnt_u[u], a.K, tau_sh[u], out, hist,
                                              a.perm, a.id_base, nn);
             if (lane == 0 && kth) atomicMax(&gtau_g[u], (unsigned long long)kth);
             if (a.lcnt) {                                  // K3 reads nn entries: no padding
